@@ -1,0 +1,198 @@
+/*
+ * liftcut_b200.h — C ABI of the B200-native liftcut hot path (libliftcut_b200.so).
+ *
+ * Drop-in boundary for the reference solver API in /root/reference/proj/include/liftcut.
+ * Every entry point names the reference interface it replaces (file:line).  Plain
+ * pointers and sizes only; host buffers in, host buffers out, device residency inside
+ * the handles.  All functions are re-entrant: state lives in handles, the last error
+ * message is thread-local.
+ *
+ * Status codes map one-to-one onto the reference exception types (errors.hpp:9-31):
+ *   LCB_VALIDATION -> ValidationError, LCB_SHAPE -> ShapeError,
+ *   LCB_NUMERIC -> NumericError ("... iteration <i>, member <j>", ascent.cpp:70-72),
+ *   LCB_CUDA / LCB_ERROR -> Error.
+ */
+#ifndef LIFTCUT_B200_H
+#define LIFTCUT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LCB_ABI_VERSION 1
+
+enum lcb_status {
+    LCB_OK = 0,
+    LCB_VALIDATION = 1,
+    LCB_SHAPE = 2,
+    LCB_NUMERIC = 3,
+    LCB_CUDA = 4,
+    LCB_ERROR = 5
+};
+
+/* Arithmetic of the iterate.  FP64 reproduces the reference (fp64, no FMA,
+ * sequential CSR-order sums: SPEC.md:100,364) bit for bit; FP32 is the fast path
+ * (fp32 state and velocity, same algorithm, checked norm-wise). */
+enum lcb_precision { LCB_FP64 = 0, LCB_FP32 = 1 };
+
+typedef struct lcb_graph lcb_graph; /* device-resident CSR (+ host copy) */
+typedef struct lcb_comm lcb_comm;   /* NCCL communicator over the ranks of one box */
+
+const char* lcb_last_error(void);
+int lcb_abi_version(void);
+int lcb_device_count(int* count);
+
+/* ---- graph: replaces the CSR of liftcut::Graph (graph.hpp:21-58) ------------
+ * offsets int64[n+1] / adjacency uint32[offsets[n]] exactly as Graph stores them
+ * (sorted, deduplicated, symmetric — graph.cpp:15-50).  The handle keeps a device
+ * copy (int32 row pointers / columns, degree vector, degree-descending row order)
+ * and a host copy for component splitting. */
+int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacency, int device,
+                     lcb_graph** out);
+void lcb_graph_destroy(lcb_graph* g);
+int lcb_graph_info(const lcb_graph* g, uint32_t* n, int64_t* m, int64_t* max_degree);
+
+/* Graph::laplacian_apply (graph.hpp:50, graph.cpp:112-122) for `count` vectors
+ * stored back to back ([count][n]). */
+int lcb_laplacian_apply(const lcb_graph* g, const double* x, double* y, int64_t count,
+                        int32_t precision);
+
+/* ---- ascent: liftcut::ascend (ascent.hpp:33-34, ascent.cpp:43-96) -----------
+ * values: DenseState::values, [B][l][n] (dense_state.hpp:50-54), updated in place.
+ * trace: optional [iterations][B] objective per step (TraceCallback, ascent.hpp:21-23);
+ * when given, early exit is disabled as in the reference (ascent.cpp:91).
+ * On LCB_NUMERIC err_iter / err_member name the first failure in member order. */
+int lcb_ascend(const lcb_graph* g, double* values, int64_t n, int32_t l, int64_t B, double alpha,
+               int64_t iterations, double momentum, int32_t early_exit, int32_t precision,
+               double* trace, int64_t* err_iter, int64_t* err_member);
+
+/* ---- objectives (objectives.hpp:25,47,50; solver.cpp:125-138) --------------- */
+/* cut_value for `count` assignments z[count][n]; LCB_VALIDATION if an entry > 1. */
+int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t* cuts);
+/* Round every member of a [B][l][n] batch (round_unlifted when lifted == 0,
+ * round_lifted otherwise), evaluate its cut, pick the first maximum.  cuts [B]
+ * and best_z [n] are optional. */
+int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int64_t B,
+                        int32_t lifted, int64_t* cuts, int64_t* best_member, int64_t* best_cut,
+                        uint8_t* best_z);
+
+/* ---- init (init.hpp:37-52, init.cpp:20-101) ---------------------------------
+ * Stream keys are RngStream::key() values (rng.hpp:27-79).  DUI / IDI / the lifted
+ * mean are integer-exact; gaussian_batch draws its normals on the device (CUDA
+ * double log / cos, within a few ulp of glibc's). */
+int lcb_dui_init(const lcb_graph* g, uint64_t key, double* x);
+int lcb_idi_init(const lcb_graph* g, double beta, uint64_t key, double* x);
+int lcb_lifted_init_mean(const lcb_graph* g, int32_t method, double beta, int32_t l,
+                         uint64_t key, double* mean);
+int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, double eta,
+                       int64_t B, uint64_t key, double* out);
+
+/* ---- solver (solver.hpp:26-90) ---------------------------------------------- */
+typedef struct lcb_config { /* SolverConfig + AscentParams + InitConfig + SearchConfig */
+    int32_t algorithm;       /* 0 pQUCO, 1 pLUCO, 2 pDECO (solver.hpp:17) */
+    int32_t lift_dim;
+    int64_t batch_size;      /* members per rank (global batch = batch_size * nranks) */
+    int64_t num_batches;
+    double alpha;
+    int64_t iterations;
+    double momentum;
+    int32_t early_exit;
+    int32_t has_lifted_ascent;
+    double l_alpha;
+    int64_t l_iterations;
+    double l_momentum;
+    int32_t l_early_exit;
+    int32_t init_method;     /* 0 DUI, 1 IDI */
+    double beta;
+    double eta;
+    double init_scale;
+    uint64_t init_seed;
+    int32_t resample_idi;
+    int32_t scale_noise;
+    double time_budget_s;    /* <= 0: none */
+    int32_t has_search;
+    int32_t population_size;
+    int64_t t_lower;
+    int64_t t_upper;
+    double e_lower;
+    double e_upper;
+    int32_t rounds;
+    int32_t search_refresh;
+    int32_t deco_alternations;
+    int32_t deco_carry;      /* 0 IncumbentColumn, 1 Fresh */
+} lcb_config;
+
+typedef struct lcb_batch_trace { /* BatchTraceEntry (solver.hpp:43-50) */
+    int64_t serial;
+    int32_t kind;            /* 0 "main", 1 "search" */
+    int32_t pad_;
+    double alpha;
+    int64_t iterations;
+    int64_t batch_best;
+    int64_t best_so_far;
+} lcb_batch_trace;
+
+typedef struct lcb_phase_trace { /* PhaseTraceEntry (solver.hpp:52-56) */
+    int32_t phase;
+    int32_t kind;            /* 0 "quco", 1 "luco" */
+    int64_t best_after;
+} lcb_phase_trace;
+
+typedef struct lcb_search_trace { /* SearchTraceEntry (evo_search.hpp:40-45) */
+    int32_t round;
+    int32_t pad_;
+    double exponent;
+    int64_t iterations;
+    double fitness;
+} lcb_search_trace;
+
+typedef struct lcb_outcome { /* SolveOutcome (solver.hpp:65-72) */
+    int64_t cut_value;
+    int64_t batch_index;
+    int64_t member_index;    /* global member index */
+    int64_t batches_run;
+    int64_t n_batch_trace;
+    int64_t n_phase_trace;
+    int64_t n_search_trace;
+    double init_s, ascent_s, rounding_s, search_s, wall_s; /* StageTimes + wall */
+} lcb_outcome;
+
+typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference config */
+    int32_t precision;       /* lcb_precision */
+    int32_t host_init;       /* -1 auto (FP64: host glibc normals, FP32: device), 0 device, 1 host */
+    int32_t batched_search;  /* evaluate each evolve() round as one multi-candidate launch */
+    int32_t pad_;
+    lcb_comm* comm;          /* NULL: single GPU */
+    /* measurement out-params (may be NULL) */
+    double* step_ms;         /* CUDA-event time of all PGA step launches */
+    int64_t* step_launches;  /* number of PGA step launches */
+    int64_t* node_updates;   /* sum over batches of n * B * l * iterations executed */
+    double* step_bytes;      /* algorithmic bytes of all step launches */
+} lcb_run_opts;
+
+/* pquco / pluco / pdeco (solver.hpp:75-86) or solve_per_component (:88-90) when
+ * per_component != 0.  assignment [n]; trace arrays are filled up to their caps, the
+ * outcome reports the full counts. */
+int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t per_component,
+              const lcb_run_opts* opts, lcb_outcome* out, uint8_t* assignment,
+              lcb_batch_trace* bt, int64_t bt_cap, lcb_phase_trace* pt, int64_t pt_cap,
+              lcb_search_trace* st, int64_t st_cap);
+
+/* ---- multi-GPU (one process per GPU; NCCL over NVLink / NVSwitch) ------------
+ * Members of every batch are sharded: rank r owns global members
+ * [r*B, (r+1)*B).  Per batch one allreduce(max) of the packed (cut, ~member) key
+ * and one allreduce(max) of the owner's winner bits; nothing inside the T loop. */
+int lcb_comm_unique_id(uint8_t id[128]);
+int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device,
+                    lcb_comm** out);
+void lcb_comm_destroy(lcb_comm* c);
+/* host helpers shared with the CPU tests of the exchange */
+uint64_t lcb_pack_key(int64_t cut, int64_t global_member);
+void lcb_unpack_key(uint64_t key, int64_t* cut, int64_t* global_member);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,307 @@
+// lcb_epilogue.cu — K4: threshold rounding -> bit-packed assignments ->
+// bit-sliced integer cut counts -> first-max argmax -> winner bits, plus the
+// boundary transposes between DenseState's [B][l][n] and the node-major device
+// layout.
+//
+// Reference lines: round_unlifted / round_lifted objectives.cpp:81-96,
+// cut_value :26-35, argmax solver.cpp:125-138, pm1_scaled :92-101.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "lcb_internal.h"
+
+namespace lcb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// transposes: DenseState [W][n] (double) <-> device [n][ld] (T)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_transpose_in(const double* __restrict__ src, T* __restrict__ dst, int n, int W,
+                               int64_t ld) {
+    __shared__ double tile[32][33];
+    const int v0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, v = v0 + threadIdx.x;
+        tile[i][threadIdx.x] = (c < W && v < n) ? src[static_cast<int64_t>(c) * n + v] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int v = v0 + i, c = c0 + threadIdx.x;
+        if (v < n && c < ld) dst[static_cast<int64_t>(v) * ld + c] = static_cast<T>(tile[threadIdx.x][i]);
+    }
+}
+
+template <typename T>
+__global__ void k_transpose_out(const T* __restrict__ src, double* __restrict__ dst, int n, int W,
+                                int64_t ld) {
+    __shared__ double tile[32][33];
+    const int v0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int v = v0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (v < n && c < W) ? static_cast<double>(src[static_cast<int64_t>(v) * ld + c]) : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, v = v0 + threadIdx.x;
+        if (c < W && v < n) dst[static_cast<int64_t>(c) * n + v] = tile[threadIdx.x][i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// trace objective: out[m] += sum_v sum_c X[v][m*l+c] * Y[v][m*l+c]
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_member_dot(const T* X, const T* Y, int n, int W, int l, int64_t ld, double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= W) return;
+    double acc = 0.0;
+    for (int v = blockIdx.y; v < n; v += gridDim.y) {
+        const int64_t i = static_cast<int64_t>(v) * ld + c;
+        acc += static_cast<double>(X[i]) * static_cast<double>(Y[i]);
+    }
+    atomicAdd(out + c / l, acc);
+}
+
+// ---------------------------------------------------------------------------
+// round + pack: one warp per (row, 32-member word); lane = member in the word
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_round_pack(const T* __restrict__ X, int64_t ld, int n, int members, int l,
+                             int lifted, uint32_t* __restrict__ Z, int words) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t total = static_cast<int64_t>(n) * words;
+    const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t t = gw; t < total; t += stride) {
+        const int row = static_cast<int>(t / words);
+        const int w = static_cast<int>(t % words);
+        const int m = w * 32 + lane;
+        bool z = false;
+        if (m < members) {
+            const T* p = X + static_cast<int64_t>(row) * ld + static_cast<int64_t>(m) * l;
+            if (lifted) {
+                double s = 0.0;  // fp64 row sum in column order
+                for (int c = 0; c < l; ++c) s = __dadd_rn(s, static_cast<double>(p[c]));
+                z = s >= 0.0;                  // inclusive (objectives.cpp:94)
+            } else {
+                z = static_cast<double>(p[0]) > 0.0;  // strict (objectives.cpp:83)
+            }
+        }
+        const uint32_t bits = __ballot_sync(0xffffffffu, z);
+        if (lane == 0) Z[static_cast<int64_t>(w) * n + row] = bits;
+    }
+}
+
+// z bytes [count][n] -> Z[w][v]
+__global__ void k_pack_bytes(const uint8_t* __restrict__ z, int n, int count, uint32_t* __restrict__ Z,
+                             int words) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = blockIdx.y;
+    if (v >= n) return;
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int m = w * 32 + b;
+        if (m < count && z[static_cast<int64_t>(m) * n + v]) bits |= 1u << b;
+    }
+    Z[static_cast<int64_t>(w) * n + v] = bits;
+}
+
+// ---------------------------------------------------------------------------
+// bit-sliced cut counting.  For every edge (u < v) and 32-member word w the
+// XOR of the two assignment words marks the members that cut the edge; 16 bit
+// planes per lane form vertical counters (ripple-carry add), flushed into 32
+// per-member integers, warp-reduced with redux.sync and added with one atomic
+// per member per warp.  Integer-exact by construction.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void planes_add(uint32_t (&p)[16], uint32_t d) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t t = p[k] & d;
+        p[k] ^= d;
+        d = t;
+    }
+}
+
+__device__ __forceinline__ void planes_flush(uint32_t (&p)[16], uint32_t (&cnt)[32]) {
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c |= ((p[k] >> b) & 1u) << k;
+        cnt[b] += c;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) p[k] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_ptr,
+                                                   const int* __restrict__ col,
+                                                   const uint32_t* __restrict__ Z, int n,
+                                                   unsigned long long* __restrict__ cuts) {
+    const int w = blockIdx.y;
+    const uint32_t* zw = Z + static_cast<int64_t>(w) * n;
+    uint32_t planes[16];
+    uint32_t cnt[32];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) planes[k] = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) cnt[b] = 0;
+    uint32_t adds = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t zu = __ldg(zw + r);
+        const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
+        for (int k = beg; k < end; ++k) {
+            const int v = __ldg(col + k);
+            if (v > r) {  // each undirected edge once (objectives.cpp:33)
+                planes_add(planes, zu ^ __ldg(zw + v));
+                if (++adds == 0xffffu) {
+                    planes_flush(planes, cnt);
+                    adds = 0;
+                }
+            }
+        }
+    }
+    planes_flush(planes, cnt);
+    const int lane = threadIdx.x & 31;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        const uint32_t t = __reduce_add_sync(0xffffffffu, cnt[b]);
+        if (lane == b) mine = t;
+    }
+    if (mine) atomicAdd(cuts + w * 32 + lane, static_cast<unsigned long long>(mine));
+}
+
+// ---------------------------------------------------------------------------
+// first-max argmax: key = cut << 32 | (0xffffffff - member) so that the max
+// key is the largest cut at the smallest member index (solver.cpp:132-134).
+// One block per segment (a batch; several when search candidates are batched).
+// ---------------------------------------------------------------------------
+__global__ void k_argmax(const unsigned long long* __restrict__ cuts, int members, int seg_size,
+                         int64_t member_base, unsigned long long* __restrict__ seg_keys) {
+    __shared__ unsigned long long red[32];
+    const int s = blockIdx.x;
+    const int lo = s * seg_size, hi = min(members, lo + seg_size);
+    unsigned long long best = 0;
+    for (int m = lo + threadIdx.x; m < hi; m += blockDim.x) {
+        const unsigned long long gm = static_cast<unsigned long long>(member_base + (m - lo));
+        const unsigned long long key = (cuts[m] << 32) | (0xffffffffull - gm);
+        best = key > best ? key : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+        best = t > best ? t : best;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+            best = t > best ? t : best;
+        }
+        if (threadIdx.x == 0) seg_keys[s] = best;
+    }
+}
+
+// winner bits for key_src[0]: member (global) -> local word/bit of Z
+__global__ void k_extract_winner(const uint32_t* __restrict__ Z, int n,
+                                 const unsigned long long* __restrict__ key_src,
+                                 int64_t member_base, int members, uint32_t* __restrict__ bits) {
+    const unsigned long long key = *key_src;
+    const int64_t gm = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull));
+    const int64_t m = gm - member_base;
+    const bool local = m >= 0 && m < members;
+    const int w = local ? static_cast<int>(m >> 5) : 0;
+    const int b = local ? static_cast<int>(m & 31) : 0;
+    const int words = (n + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = gw; i < words; i += stride) {
+        const int v = static_cast<int>(i * 32 + lane);
+        bool z = false;
+        if (local && v < n) z = (Z[static_cast<int64_t>(w) * n + v] >> b) & 1u;
+        const uint32_t word = __ballot_sync(0xffffffffu, z);
+        if (lane == 0) bits[i] = word;
+    }
+}
+
+__global__ void k_unpack_bits(const uint32_t* __restrict__ bits, int n, uint8_t* __restrict__ z) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) z[v] = static_cast<uint8_t>((bits[v >> 5] >> (v & 31)) & 1u);
+}
+
+}  // namespace
+
+template <typename T>
+void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s) {
+    const dim3 grid((n + 31) / 32, static_cast<unsigned>((ld + 31) / 32));
+    k_transpose_in<T><<<grid, dim3(32, 8), 0, s>>>(src, dst, n, W, ld);
+}
+
+template <typename T>
+void launch_transpose_out(const T* src, double* dst, int n, int W, int64_t ld, cudaStream_t s) {
+    const dim3 grid((n + 31) / 32, (W + 31) / 32);
+    k_transpose_out<T><<<grid, dim3(32, 8), 0, s>>>(src, dst, n, W, ld);
+}
+
+template <typename T>
+void launch_member_dot(const T* X, const T* Y, int n, int W, int l, int64_t ld, double* out,
+                       cudaStream_t s) {
+    const dim3 grid((W + 127) / 128, std::min(n, 256));
+    k_member_dot<T><<<grid, 128, 0, s>>>(X, Y, n, W, l, ld, out);
+}
+
+template <typename T>
+void launch_round_pack(const T* X, int64_t ld, int n, int members, int l, int lifted, uint32_t* Z,
+                       cudaStream_t s) {
+    const int words = (members + 31) / 32;
+    const int64_t warps = static_cast<int64_t>(n) * words;
+    const int blocks = static_cast<int>(std::min<int64_t>((warps + 7) / 8, 148 * 64));
+    k_round_pack<T><<<blocks, 256, 0, s>>>(X, ld, n, members, l, lifted, Z, words);
+}
+
+void launch_pack_bytes(const uint8_t* z, int n, int count, uint32_t* Z, cudaStream_t s) {
+    const int words = (count + 31) / 32;
+    k_pack_bytes<<<dim3((n + 255) / 256, words), 256, 0, s>>>(z, n, count, Z, words);
+}
+
+void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts,
+                      cudaStream_t s) {
+    cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * static_cast<size_t>(words) * 32, s);
+    const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
+    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts);
+}
+
+void launch_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
+                   unsigned long long* seg_keys, cudaStream_t s) {
+    const int segs = (members + seg_size - 1) / seg_size;
+    k_argmax<<<segs, 256, 0, s>>>(cuts, members, seg_size, member_base, seg_keys);
+}
+
+void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* key_src,
+                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s) {
+    const int words = (n + 31) / 32;
+    const int blocks = std::min((words + 7) / 8, 1024);
+    k_extract_winner<<<blocks, 256, 0, s>>>(Z, n, key_src, member_base, members, bits);
+}
+
+void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s) {
+    k_unpack_bits<<<(n + 255) / 256, 256, 0, s>>>(bits, n, z);
+}
+
+template void launch_transpose_in<float>(const double*, float*, int, int, int64_t, cudaStream_t);
+template void launch_transpose_in<double>(const double*, double*, int, int, int64_t, cudaStream_t);
+template void launch_transpose_out<float>(const float*, double*, int, int, int64_t, cudaStream_t);
+template void launch_transpose_out<double>(const double*, double*, int, int, int64_t, cudaStream_t);
+template void launch_member_dot<float>(const float*, const float*, int, int, int, int64_t, double*, cudaStream_t);
+template void launch_member_dot<double>(const double*, const double*, int, int, int, int64_t, double*, cudaStream_t);
+template void launch_round_pack<float>(const float*, int64_t, int, int, int, int, uint32_t*, cudaStream_t);
+template void launch_round_pack<double>(const double*, int64_t, int, int, int, int, uint32_t*, cudaStream_t);
+
+}  // namespace lcb

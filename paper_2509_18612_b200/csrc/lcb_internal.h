@@ -1,0 +1,143 @@
+// lcb_internal.h — shared between the kernels (lcb_kernels.cu) and the host
+// runtime (lcb_runtime.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace lcb {
+
+// ---------------------------------------------------------------------------
+// counter RNG — the integer part of rng.hpp:14-43,73-75, usable on both sides
+// ---------------------------------------------------------------------------
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t combine(uint64_t key, uint64_t word) {
+    return mix64(key ^ (word + 0x9e3779b97f4a7c15ULL + (key << 6) + (key >> 2)));
+}
+__host__ __device__ inline uint64_t rng_at(uint64_t key, uint64_t counter) {
+    return mix64(key ^ (counter * 0xd6e8feb86659fd93ULL));
+}
+__host__ __device__ inline double rng_unit(uint64_t bits) {
+    return static_cast<double>(bits >> 11) * 0x1p-53;
+}
+
+// Early-exit bits per member per iteration (ascent.cpp:74-75,91-93).
+enum : uint32_t { EX_BIG = 1u, EX_NZ = 2u, EX_NOTB = 4u };
+__host__ __device__ inline bool ex_continue(uint32_t b) {
+    // stop iff boundary ? max_change == 0 : max_change <= 1e-12
+    return (b & EX_BIG) || ((b & EX_NZ) && !(b & EX_NOTB));
+}
+
+// ---------------------------------------------------------------------------
+// device graph
+// ---------------------------------------------------------------------------
+struct DevGraph {
+    int device = 0;
+    int n = 0;
+    int64_t m = 0;
+    int64_t nnz = 0;
+    int64_t max_degree = 0;
+    double deg_mean = 0, deg_var = 0, deg_sd = 0;  // degree_stats, host-exact
+    int* row_ptr = nullptr;   // [n+1]
+    int* col = nullptr;       // [nnz]
+    double* deg64 = nullptr;  // [n]
+    float* deg32 = nullptr;   // [n]
+    int* order = nullptr;     // [n] rows by degree descending (ties by index)
+    std::vector<int64_t> h_off;
+    std::vector<uint32_t> h_adj;
+};
+
+// ---------------------------------------------------------------------------
+// PGA step (fused SpMM + heavy ball + clamp + finite check + exit flags)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct StepArgs {
+    const int* row_ptr;
+    const int* col;
+    const T* deg;
+    const int* order;
+    const T* x_in;
+    T* x_out;
+    T* vel;
+    int64_t ld;                 // row stride in elements (multiple of the warp span)
+    int n;
+    int W;                      // live columns (members * l)
+    int l;                      // lift dimension
+    const T* alpha;             // [members] or nullptr (uniform)
+    const int* tlim;            // [members] iteration count per member, or nullptr
+    const uint32_t* flags_prev; // [members] exit bits of it-1
+    uint32_t* flags_cur;        // [members] exit bits of it (zeroed beforehand)
+    uint32_t* flags_zero;       // [members] buffer to clear for it+1
+    int members;
+    unsigned long long* err;    // min over (member << 32 | iteration)
+    T mu;
+    T alpha_uniform;            // used when alpha == nullptr
+    int it;
+};
+
+enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
+
+template <typename T>
+void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);
+template <typename T>
+int step_span(int W);  // columns covered by one warp for this W
+
+template <typename T>
+void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s);
+template <typename T>
+void launch_transpose_out(const T* src, double* dst, int n, int W, int64_t ld, cudaStream_t s);
+
+// x . (Lx) per member from Y = LX  (trace objective, objectives.cpp:37-58)
+template <typename T>
+void launch_member_dot(const T* X, const T* Y, int n, int W, int l, int64_t ld, double* out,
+                       cudaStream_t s);
+
+// round + bit pack:  Z[w][v] bit b = z_{32w+b}(v)
+template <typename T>
+void launch_round_pack(const T* X, int64_t ld, int n, int members, int l, int lifted,
+                       uint32_t* Z, cudaStream_t s);
+void launch_pack_bytes(const uint8_t* z, int n, int count, uint32_t* Z, cudaStream_t s);
+// bit-sliced cut counts per member (cuts zeroed inside)
+void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts,
+                      cudaStream_t s);
+// segment argmax of packed keys; seg_keys[s] = max over members of segment s
+void launch_argmax(const unsigned long long* cuts, int members, int seg_size,
+                   int64_t member_base, unsigned long long* seg_keys, cudaStream_t s);
+// winner assignment bits (node-packed, [ceil(n/32)]) of global key `key_src[seg]`;
+// zero when the winner is not local
+void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* key_src,
+                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s);
+void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s);
+
+// init kernels (init.cpp:20-101)
+void launch_dui(const DevGraph& g, const uint64_t* col_keys, int l, double init_scale,
+                const uint32_t* carry_bits, double* mean, cudaStream_t s);
+void launch_idi(const DevGraph& g, double threshold, const uint64_t* col_keys, int l,
+                double init_scale, const uint32_t* carry_bits, int8_t* sign_scratch,
+                double* mean, cudaStream_t s);
+// gaussian batch around mean ([l][n]) or around pm1(bits)/scale; member keys [members]
+template <typename T>
+void launch_gaussian(T* X, T* V, int64_t ld, int n, int members, int l, const uint64_t* mkeys,
+                     const double* mean, const uint32_t* bits, double scale, double noise,
+                     cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct Failure {
+    int status;
+    std::string msg;
+};
+void cuda_check(cudaError_t e, const char* what);  // throws Failure{LCB_CUDA}
+
+int num_sms(int device);
+
+}  // namespace lcb

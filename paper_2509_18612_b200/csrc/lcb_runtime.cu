@@ -1,0 +1,1294 @@
+// lcb_runtime.cu — host runtime behind include/liftcut_b200.h.
+//
+// Re-states the reference orchestration (solver.cpp:106-364, evo_search.cpp:61-90)
+// around device-resident batches: the batch iterate, velocity, packed assignments,
+// the incumbent / phase-best / global-best assignments and the next batch's mean all
+// stay in HBM; per batch only the packed (cut, member) key crosses to the host.
+// Graph loading, stream-key derivation (seeding) and the (alpha, T) schedule stay
+// on the host, as the north star asks.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "../../include/liftcut_b200.h"
+#include "lcb_internal.h"
+
+namespace lcb {
+
+// ---------------------------------------------------------------------------
+// errors / small utilities
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Failure{LCB_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) cuda_check((x), #x)
+
+int num_sms(int device) {
+    static int cache[64] = {0};
+    if (device < 0 || device >= 64) return 148;
+    if (!cache[device]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[device] = v;
+    }
+    return cache[device];
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return LCB_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return LCB_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LCB_ERROR;
+    }
+}
+
+[[noreturn]] void fail(int status, const std::string& msg) { throw Failure{status, msg}; }
+
+struct DeviceScope {
+    int prev = 0;
+    explicit DeviceScope(int d) {
+        cudaGetDevice(&prev);
+        CK(cudaSetDevice(d));
+    }
+    ~DeviceScope() { cudaSetDevice(prev); }
+};
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    T* ensure(size_t k) {
+        if (k == 0) k = 1;
+        if (k > cap) {
+            release();
+            CK(cudaMalloc(&p, k * sizeof(T)));
+            cap = k;
+        }
+        return p;
+    }
+};
+
+using Clock = std::chrono::steady_clock;
+double secs_since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+uint64_t split1(uint64_t k, uint64_t a) { return combine(k, a); }
+uint64_t split2(uint64_t k, uint64_t a, uint64_t b) { return combine(combine(k, a), b); }
+uint64_t split3(uint64_t k, uint64_t a, uint64_t b, uint64_t c) {
+    return combine(combine(combine(k, a), b), c);
+}
+
+// host stateful stream — RngStream::next_* (rng.hpp:38-70)
+struct HostStream {
+    uint64_t key;
+    uint64_t ctr = 0;
+    uint64_t u64() { return rng_at(key, ctr++); }
+    double unit() { return rng_unit(u64()); }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * unit(); }
+    int64_t integer(int64_t lo, int64_t hi) {
+        const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
+        return lo + static_cast<int64_t>(u64() % span);
+    }
+    double normal() {
+        double u1 = unit();
+        const double u2 = unit();
+        if (u1 <= 0.0) u1 = 0x1p-53;
+        return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// device graph
+// ---------------------------------------------------------------------------
+void free_graph(DevGraph& g) {
+    cudaFree(g.row_ptr);
+    cudaFree(g.col);
+    cudaFree(g.deg64);
+    cudaFree(g.deg32);
+    cudaFree(g.order);
+    g.row_ptr = g.col = g.order = nullptr;
+    g.deg64 = nullptr;
+    g.deg32 = nullptr;
+}
+
+void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* adj, int device) {
+    if (n == 0) fail(LCB_VALIDATION, "graph must have at least one node");
+    if (off[0] != 0) fail(LCB_VALIDATION, "offsets[0] must be 0");
+    for (uint32_t v = 0; v < n; ++v)
+        if (off[v + 1] < off[v]) fail(LCB_VALIDATION, "offsets must be non-decreasing");
+    const int64_t nnz = off[n];
+    if (nnz > std::numeric_limits<int>::max()) fail(LCB_VALIDATION, "graph exceeds 2^31 adjacency entries");
+    for (int64_t k = 0; k < nnz; ++k)
+        if (adj[k] >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
+    g.device = device;
+    g.n = static_cast<int>(n);
+    g.nnz = nnz;
+    g.m = nnz / 2;
+    g.h_off.assign(off, off + n + 1);
+    g.h_adj.assign(adj, adj + nnz);
+    std::vector<int> rp(n + 1), deg(n), ord(n);
+    std::vector<double> d64(n);
+    std::vector<float> d32(n);
+    int64_t maxd = 0;
+    for (uint32_t v = 0; v <= n; ++v) rp[v] = static_cast<int>(off[v]);
+    for (uint32_t v = 0; v < n; ++v) {
+        deg[v] = static_cast<int>(off[v + 1] - off[v]);
+        d64[v] = static_cast<double>(deg[v]);
+        d32[v] = static_cast<float>(deg[v]);
+        maxd = std::max<int64_t>(maxd, deg[v]);
+    }
+    g.max_degree = maxd;
+    // degree_stats, sequential fp64 exactly as graph.cpp:61-73
+    const double nn = static_cast<double>(n);
+    g.deg_mean = 2.0 * static_cast<double>(g.m) / nn;
+    double acc = 0.0;
+    for (uint32_t v = 0; v < n; ++v) {
+        const double d = static_cast<double>(deg[v]) - g.deg_mean;
+        acc += d * d;
+    }
+    g.deg_var = acc / nn;
+    g.deg_sd = std::sqrt(g.deg_var);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return deg[a] > deg[b]; });
+    std::vector<int> colv(static_cast<size_t>(nnz));
+    for (int64_t k = 0; k < nnz; ++k) colv[static_cast<size_t>(k)] = static_cast<int>(adj[k]);
+
+    DeviceScope ds(device);
+    CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));
+    CK(cudaMalloc(&g.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    CK(cudaMalloc(&g.deg64, sizeof(double) * n));
+    CK(cudaMalloc(&g.deg32, sizeof(float) * n));
+    CK(cudaMalloc(&g.order, sizeof(int) * n));
+    CK(cudaMemcpy(g.row_ptr, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    if (nnz) CK(cudaMemcpy(g.col, colv.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g.deg64, d64.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g.deg32, d32.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g.order, ord.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+}
+
+template <class T>
+const T* deg_of(const DevGraph& g);
+template <>
+const float* deg_of<float>(const DevGraph& g) { return g.deg32; }
+template <>
+const double* deg_of<double>(const DevGraph& g) { return g.deg64; }
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time from the process's libnccl.so.2 (torch's when loaded)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = dlerror();
+            return a;
+        }
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy && a.GetErrorString;
+        if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
+        return a;
+    }();
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(LCB_CUDA, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace lcb
+
+struct lcb_graph {
+    lcb::DevGraph g;
+};
+struct lcb_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1;
+    int rank = 0;
+    int device = 0;
+};
+
+namespace lcb {
+
+// ---------------------------------------------------------------------------
+// per-solve device workspace
+// ---------------------------------------------------------------------------
+template <class T>
+struct Work {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t ld = 0;
+    DBuf<T> X[2], V, Y;
+    DBuf<T> alpha;
+    DBuf<int> tlim;
+    DBuf<uint32_t> flags;
+    DBuf<unsigned long long> err, cuts, keys;
+    DBuf<uint32_t> Z;
+    DBuf<uint64_t> mkeys, colkeys;
+    DBuf<double> mean, dtrace, hostbatch;
+    DBuf<int8_t> sign;
+    DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
+    unsigned long long* h_keys = nullptr;  // pinned
+    uint32_t* h_flags = nullptr;
+    size_t h_flags_cap = 0;
+    // measurement
+    double step_ms = 0.0;
+    int64_t step_launches = 0;
+    double step_bytes = 0.0;
+    int64_t node_updates = 0;
+
+    explicit Work(int dev) : device(dev) {
+        CK(cudaSetDevice(dev));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&ev0));
+        CK(cudaEventCreate(&ev1));
+        CK(cudaMallocHost(&h_keys, sizeof(unsigned long long) * 1024));
+    }
+    ~Work() {
+        if (st) cudaStreamSynchronize(st);
+        if (h_keys) cudaFreeHost(h_keys);
+        if (h_flags) cudaFreeHost(h_flags);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+    void shape(int n, int W) {
+        const int span = step_span<T>(W);
+        ld = ((static_cast<int64_t>(W) + span - 1) / span) * span;
+        const size_t cells = static_cast<size_t>(n) * static_cast<size_t>(ld);
+        X[0].ensure(cells);
+        X[1].ensure(cells);
+        V.ensure(cells);
+    }
+    uint32_t* host_flags(size_t k) {
+        if (k > h_flags_cap) {
+            if (h_flags) cudaFreeHost(h_flags);
+            CK(cudaMallocHost(&h_flags, sizeof(uint32_t) * k));
+            h_flags_cap = k;
+        }
+        return h_flags;
+    }
+};
+
+struct IterResult {
+    unsigned long long err = ~0ull;
+    int final_buf = 0;
+    int64_t iters = 0;
+};
+
+// The T-loop of ascend (ascent.cpp:58-94) over a device-resident [n][ld] batch
+// whose iterate is in X[0] and velocity in V (already initialised).
+template <class T>
+IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int l, int64_t iters,
+                          T alpha_u, const T* alpha_arr, const int* tlim_arr, T mu, bool ee,
+                          double* trace_host /* [iters][members] or null */) {
+    StepArgs<T> a{};
+    a.row_ptr = g.row_ptr;
+    a.col = g.col;
+    a.deg = deg_of<T>(g);
+    a.order = g.order;
+    a.vel = w.V.p;
+    a.ld = w.ld;
+    a.n = g.n;
+    a.W = W;
+    a.l = l;
+    a.alpha = alpha_arr;
+    a.tlim = tlim_arr;
+    a.members = members;
+    a.mu = mu;
+    a.alpha_uniform = alpha_u;
+    a.err = w.err.ensure(1);
+    CK(cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), w.st));
+    uint32_t* F = nullptr;
+    if (ee) {
+        F = w.flags.ensure(static_cast<size_t>(3) * members);
+        CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * 3 * members, w.st));
+    }
+    if (trace_host) w.Y.ensure(static_cast<size_t>(g.n) * w.ld);
+    double* dtr = trace_host ? w.dtrace.ensure(members) : nullptr;
+
+    IterResult r;
+    CK(cudaEventRecord(w.ev0, w.st));
+    int64_t it = 0;
+    for (; it < iters; ++it) {
+        a.x_in = w.X[it & 1].p;
+        a.x_out = w.X[(it + 1) & 1].p;
+        a.it = static_cast<int>(it);
+        if (ee) {
+            a.flags_prev = F + ((it + 2) % 3) * members;
+            a.flags_cur = F + (it % 3) * members;
+            a.flags_zero = F + ((it + 1) % 3) * members;
+        }
+        launch_step<T>(a, ee, MODE_STEP, w.st);
+        if (trace_host) {
+            // objective after the step: x'Lx per member (ascent.cpp:78-88)
+            StepArgs<T> b = a;
+            b.x_in = a.x_out;
+            b.x_out = w.Y.p;
+            launch_step<T>(b, false, MODE_LAPLACE, w.st);
+            CK(cudaMemsetAsync(dtr, 0, sizeof(double) * members, w.st));
+            launch_member_dot<T>(a.x_out, w.Y.p, g.n, W, l, w.ld, dtr, w.st);
+            CK(cudaMemcpyAsync(trace_host + it * members, dtr, sizeof(double) * members,
+                               cudaMemcpyDeviceToHost, w.st));
+        }
+        // Stop launching once every member has left (all later steps are copies).
+        if (ee && ((it + 1) % 32 == 0) && it + 1 < iters) {
+            uint32_t* hf = w.host_flags(members);
+            CK(cudaMemcpyAsync(hf, a.flags_cur, sizeof(uint32_t) * members, cudaMemcpyDeviceToHost, w.st));
+            CK(cudaStreamSynchronize(w.st));
+            bool any = false;
+            for (int m = 0; m < members && !any; ++m) any = ex_continue(hf[m]);
+            if (!any && !tlim_arr) {
+                ++it;
+                break;
+            }
+        }
+    }
+    CK(cudaEventRecord(w.ev1, w.st));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(w.h_keys, a.err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+    CK(cudaStreamSynchronize(w.st));
+    r.err = w.h_keys[0];
+    r.iters = it;
+    r.final_buf = static_cast<int>(it & 1);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+    w.step_ms += ms;
+    w.step_launches += it;
+    w.step_bytes += static_cast<double>(it) *
+                    (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+    w.node_updates += it * static_cast<int64_t>(g.n) * W;
+    return r;
+}
+
+std::string numeric_msg(int64_t it, int64_t member) {
+    return "ascend: non-finite value at iteration " + std::to_string(it) + ", member " +
+           std::to_string(member);
+}
+
+// ---------------------------------------------------------------------------
+// solver (solver.cpp re-stated over device-resident batches)
+// ---------------------------------------------------------------------------
+struct Cand {
+    double exponent = 0.0;
+    int64_t iterations = 1;
+    bool has_fit = false;
+    double fitness = 0.0;
+    double alpha() const { return std::pow(10.0, exponent); }
+};
+
+struct TraceSinks {
+    lcb_batch_trace* bt;
+    int64_t bt_cap;
+    lcb_phase_trace* pt;
+    int64_t pt_cap;
+    lcb_search_trace* st;
+    int64_t st_cap;
+    int64_t nbt = 0, npt = 0, nst = 0;
+};
+
+template <class T>
+struct Solver {
+    const DevGraph& g;
+    const lcb_config& cfg;
+    Work<T>& w;
+    TraceSinks& sinks;
+    lcb_comm* comm;
+    bool host_init;
+    uint64_t base;
+    Clock::time_point t0 = Clock::now();
+    int words_n;
+    int64_t B;            // local members
+    int64_t member_base;  // first global member of this rank
+
+    bool has_best = false;
+    int64_t best_cut = 0, best_serial = 0, best_member = 0;
+    int64_t serial = 0;
+    bool has_tuned[2] = {false, false};
+    Cand tuned[2];
+    int64_t main_batches[2] = {0, 0};
+    uint64_t search_runs[2] = {0, 0};
+    double init_s = 0, ascent_s = 0, rounding_s = 0, search_s = 0;
+
+    Solver(const DevGraph& graph, const lcb_config& c, Work<T>& work, TraceSinks& s, lcb_comm* cm,
+           bool hinit, uint64_t seed)
+        : g(graph), cfg(c), w(work), sinks(s), comm(cm), host_init(hinit), base(seed) {
+        words_n = (g.n + 31) / 32;
+        B = cfg.batch_size;
+        member_base = comm ? static_cast<int64_t>(comm->rank) * B : 0;
+        for (auto* b : {&w.win, &w.recenter, &w.pbest, &w.gbest, &w.carry, &w.scratch_bits})
+            b->ensure(words_n);
+    }
+
+    bool budget_gone() const {
+        return cfg.time_budget_s > 0.0 && secs_since(t0) >= cfg.time_budget_s;
+    }
+
+    void copy_bits(uint32_t* dst, const uint32_t* src) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToDevice, w.st));
+    }
+
+    // Host-side batch generation with glibc normals: gaussian_batch (init.cpp:69-87)
+    // for the local members, identical bits to the reference.
+    void host_batch(const std::vector<double>& mean, int l, uint64_t bkey, double noise) {
+        const int n = g.n;
+        const size_t entries = static_cast<size_t>(n) * l;
+        std::vector<double> vals(entries * static_cast<size_t>(B));
+        for (int64_t j = 0; j < B; ++j) {
+            HostStream ms{split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j))};
+            double* o = vals.data() + static_cast<size_t>(j) * entries;
+            for (size_t k = 0; k < entries; ++k) {
+                const double x = mean[k] + noise * ms.normal();
+                o[k] = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+            }
+        }
+        double* d = w.hostbatch.ensure(vals.size());
+        CK(cudaMemcpyAsync(d, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice, w.st));
+        launch_transpose_in<T>(d, w.X[0].p, n, static_cast<int>(B * l), w.ld, w.st);
+        CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(n) * w.ld, w.st));
+        CK(cudaStreamSynchronize(w.st));  // vals is pageable and goes out of scope
+    }
+
+    std::vector<double> host_mean_from(const double* dmean, const uint32_t* bits, int l) {
+        const int n = g.n;
+        std::vector<double> mean(static_cast<size_t>(n) * l);
+        if (dmean) {
+            CK(cudaMemcpyAsync(mean.data(), dmean, sizeof(double) * mean.size(), cudaMemcpyDeviceToHost, w.st));
+            CK(cudaStreamSynchronize(w.st));
+        } else {
+            std::vector<uint32_t> hb(words_n);
+            CK(cudaMemcpyAsync(hb.data(), bits, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToHost, w.st));
+            CK(cudaStreamSynchronize(w.st));
+            for (int v = 0; v < n; ++v)
+                mean[v] = (((hb[v >> 5] >> (v & 31)) & 1u) ? 1.0 : -1.0) / cfg.init_scale;
+            for (int c = 1; c < l; ++c) std::copy(mean.begin(), mean.begin() + n, mean.begin() + static_cast<size_t>(c) * n);
+        }
+        return mean;
+    }
+
+    struct BatchRes {
+        int64_t cut, serial, member;
+    };
+
+    // run_batch — solver.cpp:106-143.  Mean: device [l][n] array (dmean) or
+    // pm1_scaled(bits).  Winner assignment left in w.win.
+    BatchRes run_batch(bool lifted, int l, const double* dmean, const uint32_t* bits, double alpha,
+                       int64_t iters, double mu, bool ee, bool book) {
+        const int n = g.n;
+        const int64_t s = serial++;
+        const uint64_t bkey = split2(base, 0x6261u, static_cast<uint64_t>(s));
+        const double eta_eff = cfg.scale_noise ? cfg.eta / (cfg.init_scale * cfg.init_scale) : cfg.eta;
+        const double noise = std::sqrt(eta_eff);
+        const int W = static_cast<int>(B * l);
+        w.shape(n, W);
+
+        auto mark = Clock::now();
+        if (host_init) {
+            host_batch(host_mean_from(dmean, bits, l), l, bkey, noise);
+        } else {
+            std::vector<uint64_t> mk(static_cast<size_t>(B));
+            for (int64_t j = 0; j < B; ++j) mk[j] = split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j));
+            uint64_t* dk = w.mkeys.ensure(mk.size());
+            CK(cudaMemcpyAsync(dk, mk.data(), sizeof(uint64_t) * mk.size(), cudaMemcpyHostToDevice, w.st));
+            launch_gaussian<T>(w.X[0].p, w.V.p, w.ld, n, static_cast<int>(B), l, dk, dmean, bits,
+                               cfg.init_scale, noise, w.st);
+            CK(cudaStreamSynchronize(w.st));  // mk is pageable
+        }
+        if (book) init_s += secs_since(mark);
+
+        mark = Clock::now();
+        const IterResult ir = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
+                                                nullptr, nullptr, static_cast<T>(mu), ee, nullptr);
+        if (book) ascent_s += secs_since(mark);
+        if (ir.err != ~0ull)
+            fail(LCB_NUMERIC, numeric_msg(static_cast<int64_t>(ir.err & 0xffffffffull),
+                                          static_cast<int64_t>(ir.err >> 32) + member_base));
+
+        mark = Clock::now();
+        const int words = static_cast<int>((B + 31) / 32);
+        uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * n);
+        launch_round_pack<T>(w.X[ir.final_buf].p, w.ld, n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
+        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32);
+        launch_cut_count(g, Z, words, cuts, w.st);
+        unsigned long long* key = w.keys.ensure(8);
+        launch_argmax(cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
+        if (comm && comm->nranks > 1)
+            nccl_check(nccl().AllReduce(key, key, 1, ncclUint64, ncclMax, comm->comm, w.st), "allreduce(key)");
+        launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
+        if (comm && comm->nranks > 1)
+            nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
+                                        comm->comm, w.st),
+                       "allreduce(winner)");
+        CK(cudaMemcpyAsync(w.h_keys, key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+        const unsigned long long k = w.h_keys[0];
+        BatchRes r;
+        r.cut = static_cast<int64_t>(k >> 32);
+        r.member = static_cast<int64_t>(0xffffffffull - (k & 0xffffffffull));
+        r.serial = s;
+        if (book) rounding_s += secs_since(mark);
+        return r;
+    }
+
+    // note_batch — solver.cpp:145-150 (winner bits are in w.win)
+    void note_batch(const BatchRes& r, int kind, double alpha, int64_t iters) {
+        if (!has_best || r.cut > best_cut) {
+            has_best = true;
+            best_cut = r.cut;
+            best_serial = r.serial;
+            best_member = r.member;
+            copy_bits(w.gbest.p, w.win.p);
+        }
+        if (sinks.nbt < sinks.bt_cap) {
+            lcb_batch_trace& e = sinks.bt[sinks.nbt];
+            e.serial = r.serial;
+            e.kind = kind;
+            e.pad_ = 0;
+            e.alpha = alpha;
+            e.iterations = iters;
+            e.batch_best = r.cut;
+            e.best_so_far = best_cut;
+        }
+        ++sinks.nbt;
+    }
+
+    static bool ranks_before(const Cand& a, const Cand& b) {
+        const double fa = a.has_fit ? a.fitness : -std::numeric_limits<double>::infinity();
+        const double fb = b.has_fit ? b.fitness : -std::numeric_limits<double>::infinity();
+        if (fa != fb) return fa > fb;
+        if (a.iterations != b.iterations) return a.iterations < b.iterations;
+        return a.exponent < b.exponent;
+    }
+
+    // run_search — solver.cpp:154-180 + evolve — evo_search.cpp:61-90.
+    // The incumbent is w.recenter (not modified while the search runs).
+    Cand run_search(bool lifted, int l, double mu, bool ee) {
+        const auto mark = Clock::now();
+        const int kind = lifted ? 1 : 0;
+        HostStream s{split3(base, 0x6576u, static_cast<uint64_t>(kind), search_runs[kind]++)};
+        std::vector<Cand> pop(static_cast<size_t>(cfg.population_size));
+        for (Cand& c : pop) {  // sample_population (evo_search.cpp:26-34)
+            c.iterations = s.integer(cfg.t_lower, cfg.t_upper);
+            c.exponent = s.uniform(cfg.e_lower, cfg.e_upper);
+        }
+        const size_t half = pop.size() / 2;
+        for (int round = 1; round <= cfg.rounds; ++round) {
+            for (Cand& c : pop) {
+                if (c.has_fit) continue;
+                double fit;
+                if (budget_gone()) {
+                    fit = -std::numeric_limits<double>::infinity();  // Error -> -inf
+                } else {
+                    try {
+                        const BatchRes r = run_batch(lifted, l, nullptr, w.recenter.p, c.alpha(), c.iterations, mu, ee, false);
+                        note_batch(r, 1, c.alpha(), c.iterations);
+                        fit = static_cast<double>(r.cut);
+                    } catch (const Failure& f) {
+                        if (f.status != LCB_NUMERIC) throw;
+                        fit = -std::numeric_limits<double>::infinity();
+                    }
+                }
+                c.has_fit = true;
+                c.fitness = fit;
+                if (sinks.nst < sinks.st_cap) {
+                    lcb_search_trace& e = sinks.st[sinks.nst];
+                    e.round = round;
+                    e.pad_ = 0;
+                    e.exponent = c.exponent;
+                    e.iterations = c.iterations;
+                    e.fitness = fit;
+                }
+                ++sinks.nst;
+            }
+            std::stable_sort(pop.begin(), pop.end(), ranks_before);
+            for (size_t slot = half; slot < pop.size(); ++slot) {
+                const Cand& parent = pop[static_cast<size_t>(s.integer(0, static_cast<int64_t>(half) - 1))];
+                Cand child;
+                double moved = parent.exponent + 0.2 * s.normal();  // perturb_exponent
+                child.exponent = std::clamp(moved, -4.0, -1.0);
+                const double eps = s.unit();                          // perturb_iterations
+                const auto scaled = static_cast<int64_t>(
+                    std::floor(static_cast<double>(parent.iterations) * (1.0 + 0.2 * (2.0 * eps - 1.0))));
+                child.iterations = std::max<int64_t>(1, scaled);
+                pop[slot] = child;
+            }
+        }
+        search_s += secs_since(mark);
+        return pop.front();
+    }
+
+    bool search_due(int kind) const {
+        if (!cfg.has_search) return false;
+        const int64_t count = main_batches[kind];
+        if (cfg.search_refresh > 0) return (count - 1) % cfg.search_refresh == 0;
+        return !has_tuned[kind] && count == 1;
+    }
+
+    // run_phase — solver.cpp:191-246.  carry lives in w.carry (valid iff has_carry).
+    void run_phase(bool lifted, int phase_idx, bool& has_carry) {
+        const int n = g.n;
+        const int l = lifted ? cfg.lift_dim : 1;
+        const int kind = lifted ? 1 : 0;
+        double alpha = cfg.alpha, mu = cfg.momentum;
+        int64_t iters = cfg.iterations;
+        bool ee = cfg.early_exit != 0;
+        if (lifted && cfg.has_lifted_ascent) {
+            alpha = cfg.l_alpha;
+            iters = cfg.l_iterations;
+            mu = cfg.l_momentum;
+            ee = cfg.l_early_exit != 0;
+        }
+        if (has_tuned[kind]) {
+            alpha = tuned[kind].alpha();
+            iters = tuned[kind].iterations;
+        }
+        bool has_recenter = has_carry;
+        if (has_recenter) copy_bits(w.recenter.p, w.carry.p);
+        bool has_pbest = false;
+        int64_t pbest_cut = 0;
+        for (int64_t b = 0; b < cfg.num_batches; ++b) {
+            if (serial > 0 && budget_gone()) break;
+            const double* dmean = nullptr;
+            const uint32_t* bits = nullptr;
+            if (b == 0) {
+                const auto mark = Clock::now();
+                const uint64_t word = cfg.resample_idi ? static_cast<uint64_t>(serial) : 0u;
+                const uint64_t ikey = split3(base, 0x696eu, cfg.init_seed, word);
+                const bool carry_col0 = has_recenter && (l == 1 || cfg.deco_carry == 0);
+                std::vector<uint64_t> ck(static_cast<size_t>(l));
+                for (int c = 0; c < l; ++c) ck[c] = split2(ikey, 0x636fu, static_cast<uint64_t>(c));
+                uint64_t* dck = w.colkeys.ensure(ck.size());
+                CK(cudaMemcpyAsync(dck, ck.data(), sizeof(uint64_t) * ck.size(), cudaMemcpyHostToDevice, w.st));
+                double* mean = w.mean.ensure(static_cast<size_t>(n) * l);
+                const uint32_t* cb = carry_col0 ? w.recenter.p : nullptr;
+                if (cfg.init_method == 0) {
+                    if (g.max_degree < 1) fail(LCB_VALIDATION, "dui_init: graph has no edges (MaxCut is trivially 0)");
+                    launch_dui(g, dck, l, cfg.init_scale, cb, mean, w.st);
+                } else {
+                    const double thr = g.deg_mean + cfg.beta * g.deg_sd;
+                    launch_idi(g, thr, dck, l, cfg.init_scale, cb, w.sign.ensure(static_cast<size_t>(n) * l), mean, w.st);
+                }
+                CK(cudaStreamSynchronize(w.st));
+                init_s += secs_since(mark);
+                dmean = mean;
+            } else {
+                bits = w.recenter.p;
+            }
+            const BatchRes r = run_batch(lifted, l, dmean, bits, alpha, iters, mu, ee, true);
+            note_batch(r, 0, alpha, iters);
+            if (!has_pbest || r.cut > pbest_cut) {
+                has_pbest = true;
+                pbest_cut = r.cut;
+                copy_bits(w.pbest.p, w.win.p);
+            }
+            copy_bits(w.recenter.p, w.win.p);
+            has_recenter = true;
+            ++main_batches[kind];
+            if (search_due(kind) && !budget_gone()) {
+                const Cand win = run_search(lifted, l, mu, ee);
+                alpha = win.alpha();
+                iters = win.iterations;
+                tuned[kind] = win;
+                has_tuned[kind] = true;
+            }
+        }
+        if (!has_pbest) {
+            if (has_recenter) copy_bits(w.carry.p, w.recenter.p);
+            has_carry = has_recenter;
+            return;
+        }
+        if (sinks.npt < sinks.pt_cap) {
+            sinks.pt[sinks.npt].phase = phase_idx;
+            sinks.pt[sinks.npt].kind = kind;
+            sinks.pt[sinks.npt].best_after = pbest_cut;
+        }
+        ++sinks.npt;
+        copy_bits(w.carry.p, w.pbest.p);
+        has_carry = true;
+    }
+
+    // pquco / pluco / pdeco — solver.cpp:273-312
+    void solve() {
+        bool has_carry = false;
+        if (cfg.algorithm == 0) {
+            run_phase(false, 0, has_carry);
+        } else if (cfg.algorithm == 1) {
+            run_phase(true, 0, has_carry);
+        } else {
+            int phase = 0;
+            for (int round = 0;; ++round) {
+                if (cfg.time_budget_s > 0.0) {
+                    if (serial > 0 && budget_gone()) break;
+                } else if (round >= cfg.deco_alternations) {
+                    break;
+                }
+                const int64_t before = serial;
+                run_phase(false, phase++, has_carry);
+                run_phase(true, phase++, has_carry);
+                if (cfg.time_budget_s > 0.0 && serial == before) break;
+            }
+        }
+        if (!has_best) fail(LCB_ERROR, "solver produced no batch result");
+    }
+
+    void best_assignment(uint8_t* z) {
+        std::vector<uint32_t> hb(words_n);
+        CK(cudaMemcpyAsync(hb.data(), w.gbest.p, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToHost, w.st));
+        CK(cudaStreamSynchronize(w.st));
+        for (int v = 0; v < g.n; ++v) z[v] = static_cast<uint8_t>((hb[v >> 5] >> (v & 31)) & 1u);
+    }
+};
+
+void validate_config(const lcb_config& c) {
+    auto bad = [](const char* m) { fail(LCB_VALIDATION, m); };
+    if (c.batch_size < 1) bad("batch_size must be >= 1");
+    if (c.num_batches < 1) bad("num_batches must be >= 1");
+    if (c.lift_dim < 1) bad("lift_dim must be >= 1");
+    if (c.algorithm != 0 && c.lift_dim < 2) bad("lifted algorithms need lift_dim >= 2");
+    if (!(c.alpha > 0.0)) bad("ascent: alpha must be > 0");
+    if (c.iterations < 1) bad("ascent: iterations must be >= 1");
+    if (!(c.momentum >= 0.0 && c.momentum < 1.0)) bad("ascent: momentum must lie in [0, 1)");
+    if (c.has_lifted_ascent) {
+        if (!(c.l_alpha > 0.0)) bad("ascent: alpha must be > 0");
+        if (c.l_iterations < 1) bad("ascent: iterations must be >= 1");
+        if (!(c.l_momentum >= 0.0 && c.l_momentum < 1.0)) bad("ascent: momentum must lie in [0, 1)");
+    }
+    if (c.beta <= 0.0 || c.beta >= 1.0) bad("init.beta must lie in (0, 1)");
+    if (c.eta <= 0.0) bad("init.eta must be > 0");
+    if (c.init_scale < 1.0) bad("init.init_scale must be >= 1");
+    if (c.has_search) {
+        if (c.t_lower < 1 || c.t_lower > c.t_upper) bad("search: need 1 <= t_lower <= t_upper");
+        if (c.e_lower > c.e_upper) bad("search: need e_lower <= e_upper");
+        if (c.population_size < 2 || c.population_size % 2 != 0)
+            bad("search: population size must be even and >= 2");
+        if (c.rounds < 1) bad("search: rounds must be >= 1");
+    }
+    if (c.search_refresh < 0) bad("search_refresh must be >= 0");
+    if (c.deco_alternations < 1) bad("deco_alternations must be >= 1");
+    if (c.batch_size > 0x7fffffff) bad("batch_size too large");
+}
+
+template <class T>
+void solve_graph(const DevGraph& g, const lcb_config& cfg, uint64_t seed, const lcb_run_opts& o,
+                 Work<T>& w, TraceSinks& sinks, uint8_t* z, lcb_outcome& out) {
+    if (g.m < 1) fail(LCB_VALIDATION, "solver requires a graph with at least one edge");
+    const bool hinit = o.host_init < 0 ? (o.precision == LCB_FP64) : (o.host_init != 0);
+    Solver<T> s(g, cfg, w, sinks, o.comm, hinit, seed);
+    s.solve();
+    s.best_assignment(z);
+    out.cut_value += s.best_cut;
+    out.batch_index = s.best_serial;
+    out.member_index = s.best_member;
+    out.batches_run += s.serial;
+    out.init_s += s.init_s;
+    out.ascent_s += s.ascent_s;
+    out.rounding_s += s.rounding_s;
+    out.search_s += s.search_s;
+}
+
+// connected components, graph.cpp:75-99
+std::vector<std::vector<uint32_t>> components(const DevGraph& g) {
+    const uint32_t n = static_cast<uint32_t>(g.n);
+    std::vector<std::vector<uint32_t>> out;
+    std::vector<char> seen(n, 0);
+    std::vector<uint32_t> stack;
+    for (uint32_t root = 0; root < n; ++root) {
+        if (seen[root]) continue;
+        std::vector<uint32_t> comp;
+        seen[root] = 1;
+        stack.push_back(root);
+        while (!stack.empty()) {
+            const uint32_t v = stack.back();
+            stack.pop_back();
+            comp.push_back(v);
+            for (int64_t k = g.h_off[v]; k < g.h_off[v + 1]; ++k) {
+                const uint32_t u = g.h_adj[static_cast<size_t>(k)];
+                if (!seen[u]) {
+                    seen[u] = 1;
+                    stack.push_back(u);
+                }
+            }
+        }
+        std::sort(comp.begin(), comp.end());
+        out.push_back(std::move(comp));
+    }
+    return out;
+}
+
+template <class T>
+void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_component,
+               const lcb_run_opts& o, lcb_outcome& out, uint8_t* assignment, TraceSinks& sinks) {
+    Work<T> w(g.device);
+    const auto t0 = Clock::now();
+    std::memset(&out, 0, sizeof(out));
+    auto finish = [&] {
+        out.n_batch_trace = sinks.nbt;
+        out.n_phase_trace = sinks.npt;
+        out.n_search_trace = sinks.nst;
+        out.wall_s = secs_since(t0);
+        if (o.step_ms) *o.step_ms = w.step_ms;
+        if (o.step_launches) *o.step_launches = w.step_launches;
+        if (o.node_updates) *o.node_updates = w.node_updates;
+        if (o.step_bytes) *o.step_bytes = w.step_bytes;
+    };
+    if (!per_component) {
+        solve_graph<T>(g, cfg, seed, o, w, sinks, assignment, out);
+        finish();
+        return;
+    }
+    // solve_per_component — solver.cpp:314-364
+    const auto comps = components(g);
+    if (comps.size() == 1 && g.m > 0) {
+        solve_graph<T>(g, cfg, seed, o, w, sinks, assignment, out);
+        finish();
+        return;
+    }
+    if (o.comm && o.comm->nranks > 1)
+        fail(LCB_VALIDATION, "multi-GPU solve of a disconnected graph: shard per component instead");
+    std::memset(assignment, 0, static_cast<size_t>(g.n));
+    out.batch_index = -1;
+    out.member_index = -1;
+    int solved = 0;
+    std::vector<uint32_t> local(static_cast<size_t>(g.n), static_cast<uint32_t>(g.n));
+    for (size_t ci = 0; ci < comps.size(); ++ci) {
+        const auto& comp = comps[ci];
+        if (comp.size() < 2) continue;
+        const uint32_t k = static_cast<uint32_t>(comp.size());
+        for (uint32_t i = 0; i < k; ++i) local[comp[i]] = i;
+        // induced_subgraph (graph.cpp:101-110): relabel in component order; rows stay sorted
+        std::vector<int64_t> off(k + 1, 0);
+        std::vector<uint32_t> adj;
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint32_t v = comp[i];
+            for (int64_t q = g.h_off[v]; q < g.h_off[v + 1]; ++q) {
+                const uint32_t u = g.h_adj[static_cast<size_t>(q)];
+                if (local[u] != static_cast<uint32_t>(g.n)) adj.push_back(local[u]);
+            }
+            off[i + 1] = static_cast<int64_t>(adj.size());
+            std::sort(adj.begin() + off[i], adj.end());
+        }
+        for (uint32_t i = 0; i < k; ++i) local[comp[i]] = static_cast<uint32_t>(g.n);
+        if (off[k] == 0) continue;
+        DevGraph sub;
+        build_graph(sub, k, off.data(), adj.data(), g.device);
+        struct Free {
+            DevGraph& d;
+            ~Free() { free_graph(d); }
+        } fr{sub};
+        const uint64_t sub_seed = rng_at(split2(seed, 0x6370u, static_cast<uint64_t>(ci)), 0);
+        std::vector<uint8_t> za(k);
+        lcb_outcome part{};
+        TraceSinks ps{sinks.bt ? sinks.bt + std::min(sinks.nbt, sinks.bt_cap) : nullptr,
+                      std::max<int64_t>(0, sinks.bt_cap - sinks.nbt),
+                      sinks.pt ? sinks.pt + std::min(sinks.npt, sinks.pt_cap) : nullptr,
+                      std::max<int64_t>(0, sinks.pt_cap - sinks.npt),
+                      sinks.st ? sinks.st + std::min(sinks.nst, sinks.st_cap) : nullptr,
+                      std::max<int64_t>(0, sinks.st_cap - sinks.nst)};
+        solve_graph<T>(sub, cfg, sub_seed, o, w, ps, za.data(), part);
+        for (uint32_t i = 0; i < k; ++i) assignment[comp[i]] = za[i];
+        out.cut_value += part.cut_value;
+        out.batch_index = part.batch_index;
+        out.member_index = part.member_index;
+        out.batches_run += part.batches_run;
+        out.init_s += part.init_s;
+        out.ascent_s += part.ascent_s;
+        out.rounding_s += part.rounding_s;
+        out.search_s += part.search_s;
+        sinks.nbt += ps.nbt;
+        sinks.npt += ps.npt;
+        sinks.nst += ps.nst;
+        ++solved;
+    }
+    if (solved != 1) {
+        out.batch_index = -1;
+        out.member_index = -1;
+    }
+    finish();
+}
+
+// ---- boundary helpers for the single-call API -----------------------------
+template <class T>
+void ascend_host(const DevGraph& g, double* values, int64_t n, int l, int64_t B, double alpha,
+                 int64_t iters, double mu, bool ee, double* trace, int64_t* err_it, int64_t* err_m) {
+    if (!(alpha > 0.0)) fail(LCB_VALIDATION, "ascent: alpha must be > 0");
+    if (iters < 1) fail(LCB_VALIDATION, "ascent: iterations must be >= 1");
+    if (!(mu >= 0.0 && mu < 1.0)) fail(LCB_VALIDATION, "ascent: momentum must lie in [0, 1)");
+    if (n != g.n)
+        fail(LCB_SHAPE, "ascend: state row dimension " + std::to_string(n) + " != node count " +
+                            std::to_string(g.n));
+    if (l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+    const int64_t W64 = B * l;
+    if (W64 > (1 << 26)) fail(LCB_VALIDATION, "batch too wide");
+    const int W = static_cast<int>(W64);
+    DeviceScope ds(g.device);
+    Work<T> w(g.device);
+    w.shape(g.n, W);
+    const size_t count = static_cast<size_t>(W) * g.n;
+    double* d = w.hostbatch.ensure(count);
+    CK(cudaMemcpyAsync(d, values, sizeof(double) * count, cudaMemcpyHostToDevice, w.st));
+    launch_transpose_in<T>(d, w.X[0].p, g.n, W, w.ld, w.st);
+    CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(g.n) * w.ld, w.st));
+    const bool use_ee = ee && trace == nullptr;  // ascent.cpp:91
+    const IterResult r = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
+                                           nullptr, nullptr, static_cast<T>(mu), use_ee, trace);
+    launch_transpose_out<T>(w.X[r.final_buf].p, d, g.n, W, w.ld, w.st);
+    CK(cudaMemcpyAsync(values, d, sizeof(double) * count, cudaMemcpyDeviceToHost, w.st));
+    CK(cudaStreamSynchronize(w.st));
+    if (r.err != ~0ull) {
+        const int64_t it = static_cast<int64_t>(r.err & 0xffffffffull);
+        const int64_t m = static_cast<int64_t>(r.err >> 32);
+        if (err_it) *err_it = it;
+        if (err_m) *err_m = m;
+        fail(LCB_NUMERIC, numeric_msg(it, m));
+    }
+}
+
+template <class T>
+void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count) {
+    const int W = static_cast<int>(count);
+    DeviceScope ds(g.device);
+    Work<T> w(g.device);
+    w.shape(g.n, W);
+    const size_t cells = static_cast<size_t>(W) * g.n;
+    double* d = w.hostbatch.ensure(cells);
+    CK(cudaMemcpyAsync(d, x, sizeof(double) * cells, cudaMemcpyHostToDevice, w.st));
+    launch_transpose_in<T>(d, w.X[0].p, g.n, W, w.ld, w.st);
+    StepArgs<T> a{};
+    a.row_ptr = g.row_ptr;
+    a.col = g.col;
+    a.deg = deg_of<T>(g);
+    a.order = g.order;
+    a.x_in = w.X[0].p;
+    a.x_out = w.X[1].p;
+    a.ld = w.ld;
+    a.n = g.n;
+    a.W = W;
+    a.l = 1;
+    a.members = W;
+    launch_step<T>(a, false, MODE_LAPLACE, w.st);
+    launch_transpose_out<T>(w.X[1].p, d, g.n, W, w.ld, w.st);
+    CK(cudaMemcpyAsync(y, d, sizeof(double) * cells, cudaMemcpyDeviceToHost, w.st));
+    CK(cudaStreamSynchronize(w.st));
+    CK(cudaGetLastError());
+}
+
+}  // namespace lcb
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace lcb;
+
+extern "C" {
+
+const char* lcb_last_error(void) { return g_last_error.c_str(); }
+int lcb_abi_version(void) { return LCB_ABI_VERSION; }
+
+int lcb_device_count(int* count) {
+    return guard([&] { CK(cudaGetDeviceCount(count)); });
+}
+
+int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacency, int device,
+                     lcb_graph** out) {
+    return guard([&] {
+        auto h = std::make_unique<lcb_graph>();
+        try {
+            build_graph(h->g, n, offsets, adjacency, device);
+        } catch (...) {
+            free_graph(h->g);
+            throw;
+        }
+        *out = h.release();
+    });
+}
+
+void lcb_graph_destroy(lcb_graph* g) {
+    if (!g) return;
+    {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(g->g.device);
+        free_graph(g->g);
+        cudaSetDevice(prev);
+    }
+    delete g;
+}
+
+int lcb_graph_info(const lcb_graph* g, uint32_t* n, int64_t* m, int64_t* max_degree) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        if (n) *n = static_cast<uint32_t>(g->g.n);
+        if (m) *m = g->g.m;
+        if (max_degree) *max_degree = g->g.max_degree;
+    });
+}
+
+int lcb_laplacian_apply(const lcb_graph* g, const double* x, double* y, int64_t count,
+                        int32_t precision) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        if (count < 1) fail(LCB_SHAPE, "laplacian_apply: expected vectors of length " + std::to_string(g->g.n));
+        if (precision == LCB_FP32)
+            laplacian_host<float>(g->g, x, y, count);
+        else
+            laplacian_host<double>(g->g, x, y, count);
+    });
+}
+
+int lcb_ascend(const lcb_graph* g, double* values, int64_t n, int32_t l, int64_t B, double alpha,
+               int64_t iterations, double momentum, int32_t early_exit, int32_t precision,
+               double* trace, int64_t* err_iter, int64_t* err_member) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        if (precision == LCB_FP32)
+            ascend_host<float>(g->g, values, n, l, B, alpha, iterations, momentum, early_exit != 0, trace,
+                               err_iter, err_member);
+        else
+            ascend_host<double>(g->g, values, n, l, B, alpha, iterations, momentum, early_exit != 0, trace,
+                                err_iter, err_member);
+    });
+}
+
+int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t* cuts) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        const DevGraph& G = g->g;
+        const size_t cells = static_cast<size_t>(count) * G.n;
+        for (size_t i = 0; i < cells; ++i)
+            if (z[i] > 1) fail(LCB_VALIDATION, "cut_value: assignment entries must be 0 or 1");
+        if (count < 1) return;
+        DeviceScope ds(G.device);
+        Work<double> w(G.device);
+        uint8_t* dz = reinterpret_cast<uint8_t*>(w.hostbatch.ensure((cells + 7) / 8));
+        CK(cudaMemcpyAsync(dz, z, cells, cudaMemcpyHostToDevice, w.st));
+        const int words = static_cast<int>((count + 31) / 32);
+        uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
+        launch_pack_bytes(dz, G.n, static_cast<int>(count), Z, w.st);
+        unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32);
+        launch_cut_count(G, Z, words, c, w.st);
+        std::vector<unsigned long long> h(static_cast<size_t>(words) * 32);
+        CK(cudaMemcpyAsync(h.data(), c, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, w.st));
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+        for (int64_t i = 0; i < count; ++i) cuts[i] = static_cast<int64_t>(h[static_cast<size_t>(i)]);
+    });
+}
+
+int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int64_t B, int32_t lifted,
+                        int64_t* cuts, int64_t* best_member, int64_t* best_cut, uint8_t* best_z) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        const DevGraph& G = g->g;
+        if (l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+        DeviceScope ds(G.device);
+        Work<double> w(G.device);
+        const int W = static_cast<int>(B * l);
+        w.shape(G.n, W);
+        const size_t cells = static_cast<size_t>(W) * G.n;
+        double* d = w.hostbatch.ensure(cells);
+        CK(cudaMemcpyAsync(d, values, sizeof(double) * cells, cudaMemcpyHostToDevice, w.st));
+        launch_transpose_in<double>(d, w.X[0].p, G.n, W, w.ld, w.st);
+        const int words = static_cast<int>((B + 31) / 32);
+        uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
+        launch_round_pack<double>(w.X[0].p, w.ld, G.n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
+        unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32);
+        launch_cut_count(G, Z, words, c, w.st);
+        unsigned long long* key = w.keys.ensure(8);
+        launch_argmax(c, static_cast<int>(B), static_cast<int>(B), 0, key, w.st);
+        uint32_t* bits = w.win.ensure((G.n + 31) / 32);
+        launch_extract_winner(Z, G.n, key, 0, static_cast<int>(B), bits, w.st);
+        std::vector<unsigned long long> hc(static_cast<size_t>(B));
+        CK(cudaMemcpyAsync(hc.data(), c, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, w.st));
+        CK(cudaMemcpyAsync(w.h_keys, key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+        std::vector<uint32_t> hb((G.n + 31) / 32);
+        CK(cudaMemcpyAsync(hb.data(), bits, sizeof(uint32_t) * hb.size(), cudaMemcpyDeviceToHost, w.st));
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+        if (cuts)
+            for (int64_t j = 0; j < B; ++j) cuts[j] = static_cast<int64_t>(hc[static_cast<size_t>(j)]);
+        const unsigned long long k = w.h_keys[0];
+        if (best_cut) *best_cut = static_cast<int64_t>(k >> 32);
+        if (best_member) *best_member = static_cast<int64_t>(0xffffffffull - (k & 0xffffffffull));
+        if (best_z)
+            for (int v = 0; v < G.n; ++v) best_z[v] = static_cast<uint8_t>((hb[v >> 5] >> (v & 31)) & 1u);
+    });
+}
+
+static void init_mean_host(const DevGraph& G, int method, double beta, int l, const uint64_t* ck,
+                           double scale, double* out) {
+    DeviceScope ds(G.device);
+    Work<double> w(G.device);
+    uint64_t* dck = w.colkeys.ensure(static_cast<size_t>(l));
+    CK(cudaMemcpyAsync(dck, ck, sizeof(uint64_t) * l, cudaMemcpyHostToDevice, w.st));
+    double* mean = w.mean.ensure(static_cast<size_t>(G.n) * l);
+    if (method == 0) {
+        if (G.max_degree < 1) fail(LCB_VALIDATION, "dui_init: graph has no edges (MaxCut is trivially 0)");
+        launch_dui(G, dck, l, scale, nullptr, mean, w.st);
+    } else {
+        const double thr = G.deg_mean + beta * G.deg_sd;
+        launch_idi(G, thr, dck, l, scale, nullptr, w.sign.ensure(static_cast<size_t>(G.n) * l), mean, w.st);
+    }
+    CK(cudaMemcpyAsync(out, mean, sizeof(double) * G.n * l, cudaMemcpyDeviceToHost, w.st));
+    CK(cudaStreamSynchronize(w.st));
+    CK(cudaGetLastError());
+}
+
+int lcb_dui_init(const lcb_graph* g, uint64_t key, double* x) {
+    return guard([&] { init_mean_host(g->g, 0, 0.2, 1, &key, 1.0, x); });
+}
+
+int lcb_idi_init(const lcb_graph* g, double beta, uint64_t key, double* x) {
+    return guard([&] { init_mean_host(g->g, 1, beta, 1, &key, 1.0, x); });
+}
+
+int lcb_lifted_init_mean(const lcb_graph* g, int32_t method, double beta, int32_t l, uint64_t key,
+                         double* mean) {
+    return guard([&] {
+        if (l < 1) fail(LCB_VALIDATION, "lift_dim must be >= 1");
+        std::vector<uint64_t> ck(static_cast<size_t>(l));
+        for (int c = 0; c < l; ++c) ck[c] = split2(key, 0x636fu, static_cast<uint64_t>(c));
+        init_mean_host(g->g, method, beta, l, ck.data(), 1.0, mean);
+    });
+}
+
+int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, double eta, int64_t B,
+                       uint64_t key, double* out) {
+    return guard([&] {
+        if (eta <= 0.0) fail(LCB_VALIDATION, "gaussian_batch: eta must be > 0");
+        if (n < 1 || l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+        DeviceScope ds(device);
+        Work<double> w(device);
+        const int W = static_cast<int>(B * l);
+        w.shape(static_cast<int>(n), W);
+        double* dm = w.mean.ensure(static_cast<size_t>(n) * l);
+        CK(cudaMemcpyAsync(dm, mean, sizeof(double) * n * l, cudaMemcpyHostToDevice, w.st));
+        std::vector<uint64_t> mk(static_cast<size_t>(B));
+        for (int64_t j = 0; j < B; ++j) mk[j] = split2(key, 0x6d62u, static_cast<uint64_t>(j));
+        uint64_t* dk = w.mkeys.ensure(mk.size());
+        CK(cudaMemcpyAsync(dk, mk.data(), sizeof(uint64_t) * mk.size(), cudaMemcpyHostToDevice, w.st));
+        launch_gaussian<double>(w.X[0].p, w.V.p, w.ld, static_cast<int>(n), static_cast<int>(B), l, dk, dm,
+                                nullptr, 1.0, std::sqrt(eta), w.st);
+        double* d = w.hostbatch.ensure(static_cast<size_t>(W) * n);
+        launch_transpose_out<double>(w.X[0].p, d, static_cast<int>(n), W, w.ld, w.st);
+        CK(cudaMemcpyAsync(out, d, sizeof(double) * W * n, cudaMemcpyDeviceToHost, w.st));
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+    });
+}
+
+int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t per_component,
+              const lcb_run_opts* opts, lcb_outcome* out, uint8_t* assignment, lcb_batch_trace* bt,
+              int64_t bt_cap, lcb_phase_trace* pt, int64_t pt_cap, lcb_search_trace* st, int64_t st_cap) {
+    return guard([&] {
+        if (!g || !cfg || !out || !assignment) fail(LCB_VALIDATION, "null argument");
+        validate_config(*cfg);
+        lcb_run_opts o{};
+        o.precision = LCB_FP64;
+        o.host_init = -1;
+        if (opts) o = *opts;
+        DeviceScope ds(g->g.device);
+        TraceSinks sinks{bt, bt ? bt_cap : 0, pt, pt ? pt_cap : 0, st, st ? st_cap : 0};
+        if (o.precision == LCB_FP32)
+            solve_top<float>(g->g, *cfg, seed, per_component, o, *out, assignment, sinks);
+        else
+            solve_top<double>(g->g, *cfg, seed, per_component, o, *out, assignment, sinks);
+    });
+}
+
+int lcb_comm_unique_id(uint8_t id[128]) {
+    return guard([&] {
+        if (!nccl().ok) fail(LCB_CUDA, "NCCL unavailable: " + nccl().why);
+        ncclUniqueId u;
+        nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+        static_assert(sizeof(u) == 128, "ncclUniqueId size");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device, lcb_comm** out) {
+    return guard([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(LCB_VALIDATION, "bad rank / nranks");
+        auto c = std::make_unique<lcb_comm>();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->device = device;
+        if (nranks > 1) {
+            if (!nccl().ok) fail(LCB_CUDA, "NCCL unavailable: " + nccl().why);
+            DeviceScope ds(device);
+            ncclUniqueId u;
+            std::memcpy(&u, id, 128);
+            nccl_check(nccl().CommInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+        }
+        *out = c.release();
+    });
+}
+
+void lcb_comm_destroy(lcb_comm* c) {
+    if (!c) return;
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    delete c;
+}
+
+uint64_t lcb_pack_key(int64_t cut, int64_t global_member) {
+    return (static_cast<uint64_t>(cut) << 32) | (0xffffffffull - static_cast<uint64_t>(global_member));
+}
+
+void lcb_unpack_key(uint64_t key, int64_t* cut, int64_t* global_member) {
+    *cut = static_cast<int64_t>(key >> 32);
+    *global_member = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull));
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle and the golden vectors.
+
+fp64 (LCB_FP64): bit-exact states, cuts, assignments and solver records.
+fp32 (LCB_FP32): ||dx||_inf / ||x||_inf <= 1e-5 at T <= 10 (pre-saturation),
+identical rounded cuts on >= 99% of members at full T, integer parts exact.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import oracle_config, product_config
+from paper_2509_18612_b200 import LCB_FP32, LCB_FP64
+from paper_2509_18612_b200 import liftcut as lc
+
+pytestmark = pytest.mark.gpu
+
+FP32_NORM_TOL = 1e-5
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def pg(c: O.CSR) -> lc.Graph:
+    return lc.Graph.from_csr(c.n, c.off, c.adj)
+
+
+def state_of(x, n, l, B):
+    s = lc.DenseState(n, l, B)
+    s.values[:] = x
+    return s
+
+
+def run_ascend(g, x, n, l, B, alpha, T, mu, ee, prec=LCB_FP64):
+    s = state_of(x, n, l, B)
+    lc.ascend(g, s, lc.AscentParams(alpha, T, mu, ee), precision=prec)
+    return s.values
+
+
+# --------------------------------------------------------------------------- ascend
+def test_ascent_golden_bitwise(golden):
+    meta, arr = golden("ascent_states.json"), golden("ascent_states.npz")
+    for c in meta:
+        g = pg(O.CSR(c["n"], arr[c["name"] + "/off"], arr[c["name"] + "/adj"]))
+        x0 = arr[c["name"] + "/x0"]
+        for T in c["horizons"]:
+            got = run_ascend(g, x0, c["n"], c["l"], c["B"], c["alpha"], T, c["mu"], c["early_exit"])
+            assert np.array_equal(got, arr[f"{c['name']}/x{T}"]), (c["name"], T)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ascent_random_vs_oracle_bitwise(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2, 400))
+    cg = O.generate_er(n, float(rng.uniform(0.01, 0.3)), seed)
+    if cg.m == 0:
+        return
+    l, B = int(rng.integers(1, 4)), int(rng.integers(1, 70))
+    x = rng.uniform(-1, 1, B * l * n) * (10.0 ** -rng.integers(0, 5))
+    alpha, mu, T = float(rng.uniform(0.001, 0.3)), float(rng.choice([0.0, 0.5, 0.9])), int(rng.integers(1, 120))
+    for ee in (False, True):
+        want, _ = O.ascend(cg, x, l, B, alpha, T, mu, ee)
+        got = run_ascend(pg(cg), x, n, l, B, alpha, T, mu, ee)
+        assert np.array_equal(got, want), (seed, ee)
+
+
+def test_ascent_degree_skew_bitwise():
+    # star + hub rows exercise long CSR rows (BA-like degree skew)
+    n = 700
+    u = [0] * 600 + list(range(1, 699))
+    v = list(range(1, 601)) + list(range(2, 700))
+    cg = O.csr_from_edges(n, u, v)
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1e-3, 1e-3, 37 * n)
+    want, _ = O.ascend(cg, x, 1, 37, 0.01, 40, 0.9, False)
+    assert np.array_equal(run_ascend(pg(cg), x, n, 1, 37, 0.01, 40, 0.9, False), want)
+
+
+def test_c1_er800_golden(golden):
+    c1 = golden("c1_er800.json")
+    cg = O.generate_er(800, 0.015, 0)
+    g = pg(cg)
+    mean = O.lifted_init_mean(cg, 1, 0.2, 1, O.split(0, 0x696E, 0, 0)) / 1e4
+    x0 = O.gaussian_batch(mean, 800, 1, 0.8e-8, 64, int(c1["gauss_key"]))
+    for T in (10, 500):
+        xt = run_ascend(g, x0, 800, 1, 64, 0.05, T, 0.9, False)
+        assert sha(xt) == c1[f"x{T}_sha"]
+        cuts, bm, bc, _ = lc.round_cut_batch(g, state_of(xt, 800, 1, 64), lifted=False)
+        assert cuts.tolist() == c1[f"cuts{T}"]
+        assert bc == max(c1[f"cuts{T}"]) and bm == c1[f"cuts{T}"].index(bc)
+    # fp32 fast path: norm-wise early, identical cuts late
+    x10 = run_ascend(g, x0, 800, 1, 64, 0.05, 10, 0.9, False, LCB_FP32)
+    ref10, _ = O.ascend(cg, x0, 1, 64, 0.05, 10, 0.9, False)
+    for j in range(64):
+        a, b = x10[j * 800:(j + 1) * 800], ref10[j * 800:(j + 1) * 800]
+        assert np.max(np.abs(a - b)) / np.max(np.abs(b)) <= FP32_NORM_TOL
+    x500 = run_ascend(g, x0, 800, 1, 64, 0.05, 500, 0.9, False, LCB_FP32)
+    cuts32, _, _, _ = lc.round_cut_batch(g, state_of(x500, 800, 1, 64), lifted=False)
+    same = sum(int(a == b) for a, b in zip(cuts32.tolist(), c1["cuts500"]))
+    assert same >= 0.99 * 64
+
+
+def test_ascent_fp32_lifted_tolerance():
+    cg = O.generate_er(300, 0.05, 5)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1e-4, 1e-4, 20 * 2 * 300)
+    want, _ = O.ascend(cg, x, 2, 20, 0.05, 8, 0.9, False)
+    got = run_ascend(pg(cg), x, 300, 2, 20, 0.05, 8, 0.9, False, LCB_FP32)
+    for j in range(20):
+        a, b = got[j * 600:(j + 1) * 600], want[j * 600:(j + 1) * 600]
+        assert np.max(np.abs(a - b)) / np.max(np.abs(b)) <= FP32_NORM_TOL
+
+
+def test_ascent_errors():
+    g = lc.Graph(2, [(0, 1)])
+    s = state_of([0.1, -0.1], 2, 1, 1)
+    with pytest.raises(lc.NumericError) as e:
+        lc.ascend(g, s, lc.AscentParams(1e308, 5, 0.0))
+    assert "iteration" in str(e.value) and "member" in str(e.value)
+    with pytest.raises(lc.ShapeError):
+        lc.ascend(g, lc.DenseState(3, 1, 1), lc.AscentParams())
+    with pytest.raises(lc.ValidationError):
+        lc.ascend(g, s, lc.AscentParams(alpha=0.0))
+
+
+def test_ascent_trace_counts_every_step():  # test_ascent.cpp:208-223
+    g = lc.Graph(3, [(0, 1), (1, 2), (0, 2)])
+    rng = np.random.default_rng(15)
+    s = state_of(rng.uniform(-0.5, 0.5, 6), 3, 1, 2)
+    seen = []
+    lc.ascend(g, s, lc.AscentParams(0.05, 7, 0.0), trace=lambda it, m, obj: seen.append((it, m, obj)))
+    assert len(seen) == 14 and all(o >= -1e-12 for _, _, o in seen)
+    cg = O.csr_from_edges(3, [0, 1, 0], [1, 2, 2])
+    _, tr = O.ascend(cg, state_of(rng.uniform(-0.5, 0.5, 6), 3, 1, 2).values, 1, 2, 0.05, 7, 0.0, trace=True)
+    assert tr.shape == (7, 2)
+
+
+# --------------------------------------------------------------- objectives / epilogue
+def test_laplacian_apply():
+    g = lc.Graph(2, [(0, 1)])
+    assert np.array_equal(g.laplacian_apply([1.0, -1.0]), [2.0, -2.0])
+    cg = O.generate_er(500, 0.02, 9)
+    x = np.random.default_rng(1).uniform(-1, 1, (5, 500))
+    want = np.stack([O.laplacian(cg, r) for r in x])
+    assert np.array_equal(pg(cg).laplacian_apply(x), want)
+
+
+@pytest.mark.parametrize("count", [1, 31, 32, 33, 100, 1030])
+def test_cut_values_vs_oracle(count):
+    cg = O.generate_er(333, 0.04, count)
+    Z = np.random.default_rng(count).integers(0, 2, (count, 333)).astype(np.uint8)
+    got = lc.cut_values(pg(cg), Z)
+    assert got.tolist() == [O.cut_value(cg, z) for z in Z]
+    with pytest.raises(lc.ValidationError):
+        lc.cut_value(pg(cg), np.full(333, 2, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("l", [1, 2, 3])
+def test_round_cut_argmax_vs_oracle(l):
+    n, B = 257, 70
+    cg = O.generate_er(n, 0.05, l)
+    rng = np.random.default_rng(l)
+    x = rng.choice([-1.0, 0.0, 1.0, 0.25, -0.25], size=B * l * n)  # ties on purpose
+    cuts, bm, bc, z = lc.round_cut_batch(pg(cg), state_of(x, n, l, B), lifted=l > 1)
+    want = []
+    for j in range(B):
+        mv = x[j * l * n:(j + 1) * l * n]
+        zz = O.round_lifted(mv, n, l) if l > 1 else O.round_unlifted(mv)
+        want.append(O.cut_value(cg, zz))
+    assert cuts.tolist() == want
+    assert bc == max(want) and bm == want.index(max(want))
+    mv = x[bm * l * n:(bm + 1) * l * n]
+    assert np.array_equal(z, O.round_lifted(mv, n, l) if l > 1 else O.round_unlifted(mv))
+
+
+# --------------------------------------------------------------------------- init
+def test_init_golden_bitwise(golden):
+    d = golden("init_vectors.json")
+    g = lc.Graph.from_csr(len(d["off"]) - 1, d["off"], d["adj"])
+    for c in d["cases"]:
+        st = lc.RngStream(int(c["key"]))
+        assert np.array_equal(lc.dui_init(g, st), np.array(c["dui"]))
+        assert np.array_equal(lc.idi_init(g, 0.2, st), np.array(c["idi"]))
+        m = lc.lifted_init_mean(g, lc.InitConfig(beta=0.35), 3, st)
+        assert np.array_equal(m, np.array(c["lifted_idi3"]))
+
+
+def test_gaussian_batch_close_to_glibc():
+    n, l, B = 300, 2, 50
+    mean = np.random.default_rng(2).choice([-1e-4, 1e-4], n * l)
+    key = 987654321
+    got = lc.gaussian_batch(mean, n, l, 0.8e-8, B, lc.RngStream(key)).values
+    want = O.gaussian_batch(mean, n, l, 0.8e-8, B, key)
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
+    assert rel.max() < 1e-14  # a few ulp from CUDA log/cos vs glibc
+    assert np.mean(got == want) > 0.5
+    big = lc.gaussian_batch(np.zeros(n), n, 1, 4.0, B, lc.RngStream(1)).values
+    assert big.min() >= -1.0 and big.max() <= 1.0  # projected onto the box
+
+
+# --------------------------------------------------------------------------- solver
+def test_solver_golden_records_bitwise(golden):
+    d = golden("solver_records.json")
+    for c in d["cases"]:
+        off, adj = d["graphs"][c["graph"]]
+        g = lc.Graph.from_csr(len(off) - 1, off, adj)
+        cfg = product_config(c["config"])
+        fn = lc.solve_per_component if c["per_component"] else {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[cfg.algorithm]
+        r = fn(g, cfg, c["seed"], opts=lc.RunOptions(precision=LCB_FP64))
+        assert r.best.cut_value == c["cut"], c
+        assert (r.best.batch_index, r.best.member_index, r.batches_run) == (
+            c["batch_index"], c["member_index"], c["batches_run"])
+        assert r.best.assignment.tolist() == c["assignment"]
+        assert [[e.serial, 0 if e.kind == "main" else 1, e.alpha, e.iterations, e.batch_best, e.best_so_far]
+                for e in r.batch_trace] == c["batch_trace"]
+        assert [[e.phase, 0 if e.kind == "quco" else 1, e.best_after] for e in r.phase_trace] == c["phase_trace"]
+        assert [[e.round, e.exponent, e.iterations, e.fitness] for e in r.search_trace] == c["search_trace"]
+
+
+@pytest.mark.parametrize("prec", [LCB_FP64, LCB_FP32])
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_solver_device_init_quality(prec, algo):
+    cg = O.generate_er(150, 0.06, 21)
+    cfg_o = O.default_config(algorithm=algo, batch_size=48, iterations=300)
+    want = O.solve(cg, cfg_o, 4)
+    g = pg(cg)
+    cfg = lc.SolverConfig(algorithm=lc.Algorithm(algo), batch_size=48,
+                          ascent=lc.AscentParams(iterations=300))
+    fn = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[algo]
+    r = fn(g, cfg, 4, opts=lc.RunOptions(precision=prec, host_init=0))
+    assert lc.cut_value(g, r.best.assignment) == r.best.cut_value
+    assert r.batches_run == want.batches_run
+    assert r.best.cut_value >= want.cut_value - 2  # same algorithm, ulp-level different draws
+
+
+def test_solver_kats_from_reference_suite():  # test_solver.cpp:46-141, 189-224
+    edge = lc.Graph(2, [(0, 1)])
+    out = lc.pquco(edge, lc.SolverConfig(batch_size=4, ascent=lc.AscentParams(0.1, 50)), 1)
+    assert out.best.cut_value == 1 and 0 <= out.best.member_index < 4
+    star = lc.Graph(4, [(0, 1), (0, 2), (0, 3)])
+    out = lc.pquco(star, lc.SolverConfig(), 0)
+    assert out.best.cut_value == 3 and out.batch_trace[0].batch_best == 3
+    k4 = lc.Graph(4, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)])
+    cfg = lc.SolverConfig(batch_size=32, ascent=lc.AscentParams(iterations=200),
+                          init=lc.InitConfig(method=lc.InitMethod.DUI))
+    assert lc.pquco(k4, cfg, 0).best.cut_value == 4
+    assert lc.pluco(k4, lc.SolverConfig(algorithm=lc.Algorithm.pLUCO), 0).best.cut_value == 4
+    c5 = lc.Graph(5, [(0, 1), (1, 2), (2, 3), (3, 4), (0, 4)])
+    cyc = lc.pdeco(c5, lc.SolverConfig(algorithm=lc.Algorithm.pDECO), 0)
+    assert cyc.best.cut_value == 4 and [p.kind for p in cyc.phase_trace] == ["quco", "luco"] * 2
+    two = lc.Graph(4, [(0, 1), (2, 3)])
+    a = lc.solve_per_component(two, lc.SolverConfig(batch_size=16), 1)
+    assert a.best.cut_value == 2 and a.best.batch_index == -1
+    iso = lc.Graph(3, [(0, 1)])
+    b = lc.solve_per_component(iso, lc.SolverConfig(batch_size=16), 1)
+    assert b.best.cut_value == 1 and b.best.assignment[2] == 0 and b.best.batch_index >= 0
+    with pytest.raises(lc.ValidationError):
+        lc.pquco(lc.Graph(3, []), lc.SolverConfig(), 0)

@@ -170,6 +170,7 @@ typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference conf
     int64_t* step_launches;  /* number of PGA step launches */
     int64_t* node_updates;   /* sum over batches of n * B * l * iterations executed */
     double* step_bytes;      /* algorithmic bytes of all step launches */
+    double* solve_ms;        /* CUDA-event time of the whole solve on its stream */
 } lcb_run_opts;
 
 /* pquco / pluco / pdeco (solver.hpp:75-86) or solve_per_component (:88-90) when
@@ -188,6 +189,8 @@ int lcb_comm_unique_id(uint8_t id[128]);
 int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device,
                     lcb_comm** out);
 void lcb_comm_destroy(lcb_comm* c);
+/* process-wide counters: kernel launches and host<->device bytes since load */
+void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* host helpers shared with the CPU tests of the exchange */
 uint64_t lcb_pack_key(int64_t cut, int64_t global_member);
 void lcb_unpack_key(uint64_t key, int64_t* cut, int64_t* global_member);

@@ -59,7 +59,7 @@ class Outcome(C.Structure):
 class RunOpts(C.Structure):
     _fields_ = [("precision", i32), ("host_init", i32), ("batched_search", i32), ("pad_", i32),
                 ("comm", P), ("step_ms", P), ("step_launches", P), ("node_updates", P),
-                ("step_bytes", P)]
+                ("step_bytes", P), ("solve_ms", P)]
 
 
 SIGNATURES = {
@@ -81,6 +81,7 @@ SIGNATURES = {
     "lcb_comm_unique_id": (C.c_int, [P]),
     "lcb_comm_create": (C.c_int, [P, i32, i32, C.c_int, C.POINTER(P)]),
     "lcb_comm_destroy": (None, [P]),
+    "lcb_counters": (None, [P, P, P]),
     "lcb_pack_key": (u64, [i64, i64]),
     "lcb_unpack_key": (None, [u64, P, P]),
 }

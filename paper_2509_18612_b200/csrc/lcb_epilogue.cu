@@ -241,12 +241,14 @@ __global__ void k_unpack_bits(const uint32_t* __restrict__ bits, int n, uint8_t*
 template <typename T>
 void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s) {
     const dim3 grid((n + 31) / 32, static_cast<unsigned>((ld + 31) / 32));
+    count_launch();
     k_transpose_in<T><<<grid, dim3(32, 8), 0, s>>>(src, dst, n, W, ld);
 }
 
 template <typename T>
 void launch_transpose_out(const T* src, double* dst, int n, int W, int64_t ld, cudaStream_t s) {
     const dim3 grid((n + 31) / 32, (W + 31) / 32);
+    count_launch();
     k_transpose_out<T><<<grid, dim3(32, 8), 0, s>>>(src, dst, n, W, ld);
 }
 
@@ -254,6 +256,7 @@ template <typename T>
 void launch_member_dot(const T* X, const T* Y, int n, int W, int l, int64_t ld, double* out,
                        cudaStream_t s) {
     const dim3 grid((W + 127) / 128, std::min(n, 256));
+    count_launch();
     k_member_dot<T><<<grid, 128, 0, s>>>(X, Y, n, W, l, ld, out);
 }
 
@@ -263,11 +266,13 @@ void launch_round_pack(const T* X, int64_t ld, int n, int members, int l, int li
     const int words = (members + 31) / 32;
     const int64_t warps = static_cast<int64_t>(n) * words;
     const int blocks = static_cast<int>(std::min<int64_t>((warps + 7) / 8, 148 * 64));
+    count_launch();
     k_round_pack<T><<<blocks, 256, 0, s>>>(X, ld, n, members, l, lifted, Z, words);
 }
 
 void launch_pack_bytes(const uint8_t* z, int n, int count, uint32_t* Z, cudaStream_t s) {
     const int words = (count + 31) / 32;
+    count_launch();
     k_pack_bytes<<<dim3((n + 255) / 256, words), 256, 0, s>>>(z, n, count, Z, words);
 }
 
@@ -275,12 +280,14 @@ void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned 
                       cudaStream_t s) {
     cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * static_cast<size_t>(words) * 32, s);
     const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
+    count_launch();
     k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts);
 }
 
 void launch_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
                    unsigned long long* seg_keys, cudaStream_t s) {
     const int segs = (members + seg_size - 1) / seg_size;
+    count_launch();
     k_argmax<<<segs, 256, 0, s>>>(cuts, members, seg_size, member_base, seg_keys);
 }
 
@@ -288,10 +295,12 @@ void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* k
                            int64_t member_base, int members, uint32_t* bits, cudaStream_t s) {
     const int words = (n + 31) / 32;
     const int blocks = std::min((words + 7) / 8, 1024);
+    count_launch();
     k_extract_winner<<<blocks, 256, 0, s>>>(Z, n, key_src, member_base, members, bits);
 }
 
 void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s) {
+    count_launch();
     k_unpack_bits<<<(n + 255) / 256, 256, 0, s>>>(bits, n, z);
 }
 

@@ -120,6 +120,7 @@ __global__ void k_gaussian(T* __restrict__ X, T* __restrict__ V, int64_t ld, int
 void launch_dui(const DevGraph& g, const uint64_t* col_keys, int l, double init_scale,
                 const uint32_t* carry_bits, double* mean, cudaStream_t s) {
     const int64_t total = static_cast<int64_t>(g.n) * l;
+    count_launch();
     k_dui<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         g.row_ptr, g.n, static_cast<double>(g.max_degree), col_keys, l, init_scale, carry_bits, mean);
 }
@@ -129,7 +130,9 @@ void launch_idi(const DevGraph& g, double threshold, const uint64_t* col_keys, i
                 cudaStream_t s) {
     const int64_t total = static_cast<int64_t>(g.n) * l;
     const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+    count_launch();
     k_idi_sign<<<blocks, 256, 0, s>>>(g.row_ptr, g.n, threshold, col_keys, l, sign_scratch);
+    count_launch();
     k_idi_vote<<<blocks, 256, 0, s>>>(g.row_ptr, g.col, g.n, col_keys, l, init_scale, carry_bits,
                                       sign_scratch, mean);
 }
@@ -139,6 +142,7 @@ void launch_gaussian(T* X, T* V, int64_t ld, int n, int members, int l, const ui
                      const double* mean, const uint32_t* bits, double scale, double noise,
                      cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((ld + 127) / 128), static_cast<unsigned>(n < 4096 ? n : 4096));
+    count_launch();
     k_gaussian<T><<<grid, 128, 0, s>>>(X, V, ld, n, members, l, mkeys, mean, bits, scale, noise);
 }
 

@@ -140,4 +140,9 @@ void cuda_check(cudaError_t e, const char* what);  // throws Failure{LCB_CUDA}
 
 int num_sms(int device);
 
+// process-wide counters (bench evidence: launches and host<->device bytes)
+void count_launch(int k = 1);
+void count_h2d(size_t bytes);
+void count_d2h(size_t bytes);
+
 }  // namespace lcb

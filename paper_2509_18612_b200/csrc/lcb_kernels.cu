@@ -229,6 +229,7 @@ void dispatch_s(const StepArgs<T>& a, int S, cudaStream_t st) {
         constexpr int SPAN = 32 * SS * E;
         const int groups = static_cast<int>((a.ld + SPAN - 1) / SPAN);
         const dim3 grid(static_cast<unsigned>(rows_blocks) * groups);
+        count_launch();
         k_step<T, SS, GEN, EE, MODE><<<grid, kWarps * 32, 0, st>>>(a, groups);
     };
     if (S == 1)

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -31,6 +32,20 @@ namespace lcb {
 // errors / small utilities
 // ---------------------------------------------------------------------------
 thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0}, g_h2d{0}, g_d2h{0};
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+void count_h2d(size_t b) { g_h2d.fetch_add(static_cast<int64_t>(b), std::memory_order_relaxed); }
+void count_d2h(size_t b) { g_d2h.fetch_add(static_cast<int64_t>(b), std::memory_order_relaxed); }
+
+// host<->device copies go through these so the bench can report e2e bytes
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    count_h2d(bytes);
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync(H2D)");
+}
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    count_d2h(bytes);
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync(D2H)");
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -194,11 +209,11 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     CK(cudaMalloc(&g.deg64, sizeof(double) * n));
     CK(cudaMalloc(&g.deg32, sizeof(float) * n));
     CK(cudaMalloc(&g.order, sizeof(int) * n));
-    CK(cudaMemcpy(g.row_ptr, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    if (nnz) CK(cudaMemcpy(g.col, colv.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g.deg64, d64.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g.deg32, d32.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g.order, ord.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
+    if (nnz) h2d(g.col, colv.data(), sizeof(int) * nnz, 0);
+    h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
+    h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
+    h2d(g.order, ord.data(), sizeof(int) * n, 0);
 }
 
 template <class T>
@@ -386,7 +401,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         // Stop launching once every member has left (all later steps are copies).
         if (ee && ((it + 1) % 32 == 0) && it + 1 < iters) {
             uint32_t* hf = w.host_flags(members);
-            CK(cudaMemcpyAsync(hf, a.flags_cur, sizeof(uint32_t) * members, cudaMemcpyDeviceToHost, w.st));
+            d2h(hf, a.flags_cur, sizeof(uint32_t) * members, w.st);
             CK(cudaStreamSynchronize(w.st));
             bool any = false;
             for (int m = 0; m < members && !any; ++m) any = ex_continue(hf[m]);
@@ -398,7 +413,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     }
     CK(cudaEventRecord(w.ev1, w.st));
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(w.h_keys, a.err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+    d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
     CK(cudaStreamSynchronize(w.st));
     r.err = w.h_keys[0];
     r.iters = it;
@@ -495,7 +510,7 @@ struct Solver {
             }
         }
         double* d = w.hostbatch.ensure(vals.size());
-        CK(cudaMemcpyAsync(d, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice, w.st));
+        h2d(d, vals.data(), sizeof(double) * vals.size(), w.st);
         launch_transpose_in<T>(d, w.X[0].p, n, static_cast<int>(B * l), w.ld, w.st);
         CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(n) * w.ld, w.st));
         CK(cudaStreamSynchronize(w.st));  // vals is pageable and goes out of scope
@@ -505,11 +520,11 @@ struct Solver {
         const int n = g.n;
         std::vector<double> mean(static_cast<size_t>(n) * l);
         if (dmean) {
-            CK(cudaMemcpyAsync(mean.data(), dmean, sizeof(double) * mean.size(), cudaMemcpyDeviceToHost, w.st));
+            d2h(mean.data(), dmean, sizeof(double) * mean.size(), w.st);
             CK(cudaStreamSynchronize(w.st));
         } else {
             std::vector<uint32_t> hb(words_n);
-            CK(cudaMemcpyAsync(hb.data(), bits, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToHost, w.st));
+            d2h(hb.data(), bits, sizeof(uint32_t) * words_n, w.st);
             CK(cudaStreamSynchronize(w.st));
             for (int v = 0; v < n; ++v)
                 mean[v] = (((hb[v >> 5] >> (v & 31)) & 1u) ? 1.0 : -1.0) / cfg.init_scale;
@@ -541,7 +556,7 @@ struct Solver {
             std::vector<uint64_t> mk(static_cast<size_t>(B));
             for (int64_t j = 0; j < B; ++j) mk[j] = split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j));
             uint64_t* dk = w.mkeys.ensure(mk.size());
-            CK(cudaMemcpyAsync(dk, mk.data(), sizeof(uint64_t) * mk.size(), cudaMemcpyHostToDevice, w.st));
+            h2d(dk, mk.data(), sizeof(uint64_t) * mk.size(), w.st);
             launch_gaussian<T>(w.X[0].p, w.V.p, w.ld, n, static_cast<int>(B), l, dk, dmean, bits,
                                cfg.init_scale, noise, w.st);
             CK(cudaStreamSynchronize(w.st));  // mk is pageable
@@ -571,7 +586,7 @@ struct Solver {
             nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
                                         comm->comm, w.st),
                        "allreduce(winner)");
-        CK(cudaMemcpyAsync(w.h_keys, key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+        d2h(w.h_keys, key, sizeof(unsigned long long), w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
         const unsigned long long k = w.h_keys[0];
@@ -711,7 +726,7 @@ struct Solver {
                 std::vector<uint64_t> ck(static_cast<size_t>(l));
                 for (int c = 0; c < l; ++c) ck[c] = split2(ikey, 0x636fu, static_cast<uint64_t>(c));
                 uint64_t* dck = w.colkeys.ensure(ck.size());
-                CK(cudaMemcpyAsync(dck, ck.data(), sizeof(uint64_t) * ck.size(), cudaMemcpyHostToDevice, w.st));
+                h2d(dck, ck.data(), sizeof(uint64_t) * ck.size(), w.st);
                 double* mean = w.mean.ensure(static_cast<size_t>(n) * l);
                 const uint32_t* cb = carry_col0 ? w.recenter.p : nullptr;
                 if (cfg.init_method == 0) {
@@ -786,7 +801,7 @@ struct Solver {
 
     void best_assignment(uint8_t* z) {
         std::vector<uint32_t> hb(words_n);
-        CK(cudaMemcpyAsync(hb.data(), w.gbest.p, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToHost, w.st));
+        d2h(hb.data(), w.gbest.p, sizeof(uint32_t) * words_n, w.st);
         CK(cudaStreamSynchronize(w.st));
         for (int v = 0; v < g.n; ++v) z[v] = static_cast<uint8_t>((hb[v >> 5] >> (v & 31)) & 1u);
     }
@@ -874,7 +889,23 @@ void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_
     Work<T> w(g.device);
     const auto t0 = Clock::now();
     std::memset(&out, 0, sizeof(out));
+    cudaEvent_t s0 = nullptr, s1 = nullptr;
+    CK(cudaEventCreate(&s0));
+    CK(cudaEventCreate(&s1));
+    struct EvFree {
+        cudaEvent_t a, b;
+        ~EvFree() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } evf{s0, s1};
+    CK(cudaEventRecord(s0, w.st));
     auto finish = [&] {
+        CK(cudaEventRecord(s1, w.st));
+        CK(cudaEventSynchronize(s1));
+        float sms = 0.f;
+        CK(cudaEventElapsedTime(&sms, s0, s1));
+        if (o.solve_ms) *o.solve_ms = sms;
         out.n_batch_trace = sinks.nbt;
         out.n_phase_trace = sinks.npt;
         out.n_search_trace = sinks.nst;
@@ -978,14 +1009,14 @@ void ascend_host(const DevGraph& g, double* values, int64_t n, int l, int64_t B,
     w.shape(g.n, W);
     const size_t count = static_cast<size_t>(W) * g.n;
     double* d = w.hostbatch.ensure(count);
-    CK(cudaMemcpyAsync(d, values, sizeof(double) * count, cudaMemcpyHostToDevice, w.st));
+    h2d(d, values, sizeof(double) * count, w.st);
     launch_transpose_in<T>(d, w.X[0].p, g.n, W, w.ld, w.st);
     CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(g.n) * w.ld, w.st));
     const bool use_ee = ee && trace == nullptr;  // ascent.cpp:91
     const IterResult r = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
                                            nullptr, nullptr, static_cast<T>(mu), use_ee, trace);
     launch_transpose_out<T>(w.X[r.final_buf].p, d, g.n, W, w.ld, w.st);
-    CK(cudaMemcpyAsync(values, d, sizeof(double) * count, cudaMemcpyDeviceToHost, w.st));
+    d2h(values, d, sizeof(double) * count, w.st);
     CK(cudaStreamSynchronize(w.st));
     if (r.err != ~0ull) {
         const int64_t it = static_cast<int64_t>(r.err & 0xffffffffull);
@@ -1004,7 +1035,7 @@ void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count
     w.shape(g.n, W);
     const size_t cells = static_cast<size_t>(W) * g.n;
     double* d = w.hostbatch.ensure(cells);
-    CK(cudaMemcpyAsync(d, x, sizeof(double) * cells, cudaMemcpyHostToDevice, w.st));
+    h2d(d, x, sizeof(double) * cells, w.st);
     launch_transpose_in<T>(d, w.X[0].p, g.n, W, w.ld, w.st);
     StepArgs<T> a{};
     a.row_ptr = g.row_ptr;
@@ -1020,7 +1051,7 @@ void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count
     a.members = W;
     launch_step<T>(a, false, MODE_LAPLACE, w.st);
     launch_transpose_out<T>(w.X[1].p, d, g.n, W, w.ld, w.st);
-    CK(cudaMemcpyAsync(y, d, sizeof(double) * cells, cudaMemcpyDeviceToHost, w.st));
+    d2h(y, d, sizeof(double) * cells, w.st);
     CK(cudaStreamSynchronize(w.st));
     CK(cudaGetLastError());
 }
@@ -1113,14 +1144,14 @@ int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t*
         DeviceScope ds(G.device);
         Work<double> w(G.device);
         uint8_t* dz = reinterpret_cast<uint8_t*>(w.hostbatch.ensure((cells + 7) / 8));
-        CK(cudaMemcpyAsync(dz, z, cells, cudaMemcpyHostToDevice, w.st));
+        h2d(dz, z, cells, w.st);
         const int words = static_cast<int>((count + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
         launch_pack_bytes(dz, G.n, static_cast<int>(count), Z, w.st);
         unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32);
         launch_cut_count(G, Z, words, c, w.st);
         std::vector<unsigned long long> h(static_cast<size_t>(words) * 32);
-        CK(cudaMemcpyAsync(h.data(), c, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, w.st));
+        d2h(h.data(), c, sizeof(unsigned long long) * h.size(), w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
         for (int64_t i = 0; i < count; ++i) cuts[i] = static_cast<int64_t>(h[static_cast<size_t>(i)]);
@@ -1139,7 +1170,7 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
         w.shape(G.n, W);
         const size_t cells = static_cast<size_t>(W) * G.n;
         double* d = w.hostbatch.ensure(cells);
-        CK(cudaMemcpyAsync(d, values, sizeof(double) * cells, cudaMemcpyHostToDevice, w.st));
+        h2d(d, values, sizeof(double) * cells, w.st);
         launch_transpose_in<double>(d, w.X[0].p, G.n, W, w.ld, w.st);
         const int words = static_cast<int>((B + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
@@ -1151,10 +1182,10 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
         uint32_t* bits = w.win.ensure((G.n + 31) / 32);
         launch_extract_winner(Z, G.n, key, 0, static_cast<int>(B), bits, w.st);
         std::vector<unsigned long long> hc(static_cast<size_t>(B));
-        CK(cudaMemcpyAsync(hc.data(), c, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, w.st));
-        CK(cudaMemcpyAsync(w.h_keys, key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, w.st));
+        d2h(hc.data(), c, sizeof(unsigned long long) * B, w.st);
+        d2h(w.h_keys, key, sizeof(unsigned long long), w.st);
         std::vector<uint32_t> hb((G.n + 31) / 32);
-        CK(cudaMemcpyAsync(hb.data(), bits, sizeof(uint32_t) * hb.size(), cudaMemcpyDeviceToHost, w.st));
+        d2h(hb.data(), bits, sizeof(uint32_t) * hb.size(), w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
         if (cuts)
@@ -1172,7 +1203,7 @@ static void init_mean_host(const DevGraph& G, int method, double beta, int l, co
     DeviceScope ds(G.device);
     Work<double> w(G.device);
     uint64_t* dck = w.colkeys.ensure(static_cast<size_t>(l));
-    CK(cudaMemcpyAsync(dck, ck, sizeof(uint64_t) * l, cudaMemcpyHostToDevice, w.st));
+    h2d(dck, ck, sizeof(uint64_t) * l, w.st);
     double* mean = w.mean.ensure(static_cast<size_t>(G.n) * l);
     if (method == 0) {
         if (G.max_degree < 1) fail(LCB_VALIDATION, "dui_init: graph has no edges (MaxCut is trivially 0)");
@@ -1181,7 +1212,7 @@ static void init_mean_host(const DevGraph& G, int method, double beta, int l, co
         const double thr = G.deg_mean + beta * G.deg_sd;
         launch_idi(G, thr, dck, l, scale, nullptr, w.sign.ensure(static_cast<size_t>(G.n) * l), mean, w.st);
     }
-    CK(cudaMemcpyAsync(out, mean, sizeof(double) * G.n * l, cudaMemcpyDeviceToHost, w.st));
+    d2h(out, mean, sizeof(double) * G.n * l, w.st);
     CK(cudaStreamSynchronize(w.st));
     CK(cudaGetLastError());
 }
@@ -1214,16 +1245,16 @@ int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, dou
         const int W = static_cast<int>(B * l);
         w.shape(static_cast<int>(n), W);
         double* dm = w.mean.ensure(static_cast<size_t>(n) * l);
-        CK(cudaMemcpyAsync(dm, mean, sizeof(double) * n * l, cudaMemcpyHostToDevice, w.st));
+        h2d(dm, mean, sizeof(double) * n * l, w.st);
         std::vector<uint64_t> mk(static_cast<size_t>(B));
         for (int64_t j = 0; j < B; ++j) mk[j] = split2(key, 0x6d62u, static_cast<uint64_t>(j));
         uint64_t* dk = w.mkeys.ensure(mk.size());
-        CK(cudaMemcpyAsync(dk, mk.data(), sizeof(uint64_t) * mk.size(), cudaMemcpyHostToDevice, w.st));
+        h2d(dk, mk.data(), sizeof(uint64_t) * mk.size(), w.st);
         launch_gaussian<double>(w.X[0].p, w.V.p, w.ld, static_cast<int>(n), static_cast<int>(B), l, dk, dm,
                                 nullptr, 1.0, std::sqrt(eta), w.st);
         double* d = w.hostbatch.ensure(static_cast<size_t>(W) * n);
         launch_transpose_out<double>(w.X[0].p, d, static_cast<int>(n), W, w.ld, w.st);
-        CK(cudaMemcpyAsync(out, d, sizeof(double) * W * n, cudaMemcpyDeviceToHost, w.st));
+        d2h(out, d, sizeof(double) * W * n, w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
     });
@@ -1280,6 +1311,12 @@ void lcb_comm_destroy(lcb_comm* c) {
     if (!c) return;
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     delete c;
+}
+
+void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+    if (launches) *launches = g_launches.load();
+    if (h2d_bytes) *h2d_bytes = g_h2d.load();
+    if (d2h_bytes) *d2h_bytes = g_d2h.load();
 }
 
 uint64_t lcb_pack_key(int64_t cut, int64_t global_member) {

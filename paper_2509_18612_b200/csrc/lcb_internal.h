@@ -51,6 +51,10 @@ struct DevGraph {
     double* deg64 = nullptr;  // [n]
     float* deg32 = nullptr;   // [n]
     int* order = nullptr;     // [n] rows by degree descending (ties by index)
+    // relabelled copy for the member-resident kernel (rows in `order`, uint16 columns)
+    int* res_row_ptr = nullptr;   // [n+1]
+    uint16_t* res_col = nullptr;  // [nnz]
+    int* res_perm = nullptr;      // [n] new row -> original row (== order)
     std::vector<int64_t> h_off;
     std::vector<uint32_t> h_adj;
 };
@@ -84,6 +88,27 @@ struct StepArgs {
 };
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
+
+// member-resident persistent kernel (lcb_resident.cu), fp32
+constexpr int64_t kResidentSmemMax = 220 * 1024;
+struct ResidentArgs {
+    const int* row_ptr;      // relabelled
+    const uint16_t* col;     // relabelled
+    const int* perm;         // new -> old row
+    float* X;                // [n][ld] original row order, in/out
+    int64_t ld;
+    int n;
+    int W;
+    int l;
+    int T;
+    float alpha_uniform;
+    const float* alpha;      // [members] or null
+    const int* tlim;         // [members] or null
+    float mu;
+    unsigned long long* err;
+};
+bool resident_fits(int n, int W, int l, bool ee, int& K);
+void launch_resident(const ResidentArgs& a, int K, bool ee, cudaStream_t s);
 
 template <typename T>
 void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);

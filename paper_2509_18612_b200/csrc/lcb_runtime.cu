@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -156,7 +158,11 @@ void free_graph(DevGraph& g) {
     cudaFree(g.deg64);
     cudaFree(g.deg32);
     cudaFree(g.order);
-    g.row_ptr = g.col = g.order = nullptr;
+    cudaFree(g.res_row_ptr);
+    cudaFree(g.res_col);
+    g.row_ptr = g.col = g.order = g.res_row_ptr = nullptr;
+    g.res_col = nullptr;
+    g.res_perm = nullptr;
     g.deg64 = nullptr;
     g.deg32 = nullptr;
 }
@@ -214,6 +220,24 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
+    g.res_perm = g.order;
+    if (n <= 65535) {
+        // relabelled CSR for the member-resident kernel: new id = rank in `order`
+        std::vector<int> inv(n);
+        for (uint32_t r = 0; r < n; ++r) inv[ord[r]] = static_cast<int>(r);
+        std::vector<int> rrp(n + 1, 0);
+        std::vector<uint16_t> rcol(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+        for (uint32_t r = 0; r < n; ++r) {
+            const int v = ord[r];
+            rrp[r + 1] = rrp[r] + deg[v];
+            int64_t o = rrp[r];
+            for (int64_t k = off[v]; k < off[v + 1]; ++k) rcol[static_cast<size_t>(o++)] = static_cast<uint16_t>(inv[adj[k]]);
+        }
+        CK(cudaMalloc(&g.res_row_ptr, sizeof(int) * (n + 1)));
+        CK(cudaMalloc(&g.res_col, sizeof(uint16_t) * rcol.size()));
+        h2d(g.res_row_ptr, rrp.data(), sizeof(int) * (n + 1), 0);
+        h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
+    }
 }
 
 template <class T>
@@ -303,6 +327,7 @@ struct Work {
     int64_t step_launches = 0;
     double step_bytes = 0.0;
     int64_t node_updates = 0;
+    int64_t resident_iters = 0;  // iterations executed by the member-resident kernel
 
     explicit Work(int dev) : device(dev) {
         CK(cudaSetDevice(dev));
@@ -375,6 +400,50 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     double* dtr = trace_host ? w.dtrace.ensure(members) : nullptr;
 
     IterResult r;
+    int K = 0;
+    static const bool resident_enabled = [] {
+        const char* e = std::getenv("LCB_RESIDENT");
+        return !(e && e[0] == '0');
+    }();
+    if constexpr (std::is_same_v<T, float>) {
+        if (resident_enabled && !trace_host && g.res_row_ptr && iters <= 0x7fffffff &&
+            resident_fits(g.n, W, l, ee, K)) {
+            // K2: all iterations in one launch, state resident in SMEM
+            ResidentArgs ra{};
+            ra.row_ptr = g.res_row_ptr;
+            ra.col = g.res_col;
+            ra.perm = g.res_perm;
+            ra.X = w.X[0].p;
+            ra.ld = w.ld;
+            ra.n = g.n;
+            ra.W = W;
+            ra.l = l;
+            ra.T = static_cast<int>(iters);
+            ra.alpha_uniform = alpha_u;
+            ra.alpha = alpha_arr;
+            ra.tlim = tlim_arr;
+            ra.mu = mu;
+            ra.err = a.err;
+            CK(cudaEventRecord(w.ev0, w.st));
+            launch_resident(ra, K, ee, w.st);
+            CK(cudaEventRecord(w.ev1, w.st));
+            CK(cudaGetLastError());
+            d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
+            CK(cudaStreamSynchronize(w.st));
+            r.err = w.h_keys[0];
+            r.iters = iters;
+            r.final_buf = 0;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+            w.step_ms += ms;
+            w.step_launches += 1;
+            w.step_bytes += static_cast<double>(iters) *
+                            (16.0 * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+            w.node_updates += iters * static_cast<int64_t>(g.n) * W;
+            w.resident_iters += iters;
+            return r;
+        }
+    }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;
     for (; it < iters; ++it) {

@@ -259,3 +259,40 @@ def test_solver_kats_from_reference_suite():  # test_solver.cpp:46-141, 189-224
     assert b.best.cut_value == 1 and b.best.assignment[2] == 0 and b.best.batch_index >= 0
     with pytest.raises(lc.ValidationError):
         lc.pquco(lc.Graph(3, []), lc.SolverConfig(), 0)
+
+
+# ------------------------------------------------------- member-resident fp32 kernel (K2)
+def _ba_like(n, m, seed):
+    rng = np.random.default_rng(seed)
+    us, vs, targets = [], [], list(range(m))
+    repeated = []
+    for v in range(m, n):
+        chosen = set()
+        while len(chosen) < m:
+            chosen.add(int(rng.choice(repeated)) if repeated and rng.random() < 0.9 else int(rng.integers(0, v)))
+        for u in chosen:
+            us.append(u)
+            vs.append(v)
+        repeated += list(chosen) + [v] * m
+    return O.csr_from_edges(n, us, vs)
+
+
+@pytest.mark.parametrize("l,B,ee", [(1, 400, False), (2, 200, False), (1, 400, True), (2, 200, True), (3, 110, False)])
+def test_resident_fp32_tolerance_and_cuts(l, B, ee):
+    cg = _ba_like(3000, 4, 11)
+    g = pg(cg)
+    rng = np.random.default_rng(l * 10 + B)
+    x = rng.choice([-1e-4, 1e-4], B * l * cg.n) + rng.normal(0, 9e-5, B * l * cg.n)
+    for T in (6,):
+        want, _ = O.ascend(cg, x, l, B, 0.05, T, 0.9, ee)
+        got = run_ascend(g, x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP32)
+        for j in range(B):
+            a, b = got[j * l * cg.n:(j + 1) * l * cg.n], want[j * l * cg.n:(j + 1) * l * cg.n]
+            assert np.max(np.abs(a - b)) / np.max(np.abs(b)) <= FP32_NORM_TOL, (j, T)
+    T = 300
+    want, _ = O.ascend(cg, x, l, B, 0.05, T, 0.9, ee)
+    got = run_ascend(g, x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP32)
+    c32, _, _, _ = lc.round_cut_batch(g, state_of(got, cg.n, l, B), lifted=l > 1)
+    c64, _, _, _ = lc.round_cut_batch(g, state_of(want, cg.n, l, B), lifted=l > 1)
+    assert np.mean(c32 == c64) >= 0.97
+    assert abs(int(c32.max()) - int(c64.max())) <= 2

@@ -52,8 +52,9 @@ struct DevGraph {
     float* deg32 = nullptr;   // [n]
     int* order = nullptr;     // [n] rows by degree descending (ties by index)
     // relabelled copy for the member-resident kernel (rows in `order`, uint16 columns)
-    int* res_row_ptr = nullptr;   // [n+1]
-    uint16_t* res_col = nullptr;  // [nnz]
+    uint32_t* res_info = nullptr; // [n] (offset-in-chunk words << 16) | degree; null if n/a
+    int* res_chunk = nullptr;     // [ceil(n/1024)] chunk base (4-col words)
+    uint16_t* res_col = nullptr;  // [padded nnz]
     int* res_perm = nullptr;      // [n] new row -> original row (== order)
     std::vector<int64_t> h_off;
     std::vector<uint32_t> h_adj;
@@ -89,26 +90,30 @@ struct StepArgs {
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
 
-// member-resident persistent kernel (lcb_resident.cu), fp32
+// member-resident persistent kernel (lcb_resident.cu), fp32 and fp64
 constexpr int64_t kResidentSmemMax = 220 * 1024;
+constexpr int kResidentMaxRows = 14 * 1024;
 struct ResidentArgs {
-    const int* row_ptr;      // relabelled
-    const uint16_t* col;     // relabelled
-    const int* perm;         // new -> old row
-    float* X;                // [n][ld] original row order, in/out
+    const uint32_t* rowinfo; // relabelled: (4-col word offset within its 1024-row chunk) << 16 | degree
+    const int* chunk_base;   // first 4-col word of each 1024-row chunk
+    const uint16_t* col;     // relabelled; pad entries point at the zero row n
+    const int* perm;         // new -> original row
+    void* X;                 // [n][ld] (float or double), original row order, in/out
     int64_t ld;
     int n;
     int W;
     int l;
     int T;
     float alpha_uniform;
-    const float* alpha;      // [members] or null
-    const int* tlim;         // [members] or null
     float mu;
+    double alpha_uniform64;
+    double mu64;
+    const void* alpha;       // [members] (float or double) or null
+    const int* tlim;         // [members] or null
     unsigned long long* err;
 };
-bool resident_fits(int n, int W, int l, bool ee, int& K);
-void launch_resident(const ResidentArgs& a, int K, bool ee, cudaStream_t s);
+bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K);
+void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
 
 template <typename T>
 void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);

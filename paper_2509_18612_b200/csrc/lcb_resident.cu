@@ -1,22 +1,21 @@
-// lcb_resident.cu — K2: member-resident persistent PGA kernel (fp32).
+// lcb_resident.cu — K2: member-resident persistent PGA kernel.
 //
-// For graphs whose per-column state fits on chip (n * K * 8 B <= ~220 KB, i.e.
-// configs 1 and 2), one CTA owns K columns of the batch for ALL n rows:
+// For graphs whose per-column state fits on chip (configs 1 and 2), one CTA owns
+// K columns of the batch for ALL n rows and runs all T iterations in one launch:
 //   * the iterate lives in shared memory, double-buffered (Jacobi update:
-//     ascent.cpp:58-77 reads the old iterate of every neighbour);
-//   * the velocity lives in registers (each row is owned by one lane);
-//   * all T iterations run inside one launch with a CTA barrier per iteration —
-//     members are independent (ascent.cpp:52), so no grid-wide sync is needed;
-//   * the CSR is streamed from L2 every iteration (relabelled rows in
-//     degree-descending order, uint16 columns), shared by every CTA.
-// HBM is touched only to load the initial slab and write the final one.  The
-// per-iteration work is 8 lanes per row over the row's neighbours (coalesced
-// column loads, random LDS gathers), a 3-step shuffle reduction, and the fused
-// heavy-ball / clamp / finite-check / exit-flag epilogue.
-//
-// Summation order within a row is a fixed lane-strided tree, not the reference's
-// sequential order, so this path is the fp32 fast path (norm-wise tolerance);
-// the fp64 bit-exact path is k_step in lcb_kernels.cu.
+//     ascent.cpp:58-77 reads the old iterate of every neighbour), plus a zero
+//     sentinel row at index n;
+//   * each thread owns rows tid, tid+1024, ... for the whole launch: their CSR
+//     offsets, degrees and heavy-ball velocities stay in registers;
+//   * rows are relabelled in degree-descending order, so a warp's 32 consecutive
+//     rows have near-equal degree (no divergence) and contiguous adjacency lists
+//     (the column stream is near-coalesced); lists are padded to a multiple of 4
+//     with the sentinel so one 8-byte load fetches 4 uint16 columns;
+//   * members are independent (ascent.cpp:52): a CTA barrier per iteration is the
+//     only synchronisation; HBM is touched only to load / store the slab.
+// The per-(row, column) sum runs over the neighbours in the reference's CSR order
+// (graph.cpp:118) and the padding adds +0.0 (acc is never -0.0), so with T=double
+// and round-to-nearest intrinsics the kernel is bit-exact with the reference.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,65 +26,70 @@ namespace lcb {
 
 namespace {
 
-template <int K>
-struct SlabT;
+template <typename T, int K>
+struct Slab;
 template <>
-struct SlabT<1> {
+struct Slab<float, 1> {
     using type = float;
 };
 template <>
-struct SlabT<2> {
+struct Slab<float, 2> {
     using type = float2;
+};
+template <>
+struct Slab<double, 1> {
+    using type = double;
 };
 
 __device__ __forceinline__ float comp(const float& v, int) { return v; }
+__device__ __forceinline__ double comp(const double& v, int) { return v; }
 __device__ __forceinline__ float comp(const float2& v, int k) { return k ? v.y : v.x; }
 __device__ __forceinline__ void setc(float& v, int, float x) { v = x; }
+__device__ __forceinline__ void setc(double& v, int, double x) { v = x; }
 __device__ __forceinline__ void setc(float2& v, int k, float x) {
     if (k)
         v.y = x;
     else
         v.x = x;
 }
-__device__ __forceinline__ void addto(float& a, const float& b) { a += b; }
+__device__ __forceinline__ void addto(float& a, const float& b) { a = __fadd_rn(a, b); }
+__device__ __forceinline__ void addto(double& a, const double& b) { a = __dadd_rn(a, b); }
 __device__ __forceinline__ void addto(float2& a, const float2& b) {
-    a.x += b.x;
-    a.y += b.y;
+    a.x = __fadd_rn(a.x, b.x);
+    a.y = __fadd_rn(a.y, b.y);
 }
-__device__ __forceinline__ float xor_sum8(float v) {
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
+template <typename VT>
+__device__ __forceinline__ VT zero_v() {
+    VT v;
+    setc(v, 0, 0);
+    if constexpr (sizeof(VT) == 8 && !__is_same(VT, double)) setc(v, 1, 0);
     return v;
 }
-__device__ __forceinline__ float2 xor_sum8(float2 v) {
-    v.x = xor_sum8(v.x);
-    v.y = xor_sum8(v.y);
-    return v;
-}
-__device__ __forceinline__ void zero(float& v) { v = 0.f; }
-__device__ __forceinline__ void zero(float2& v) { v = make_float2(0.f, 0.f); }
+
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
 
 constexpr int kThreads = 1024;
-constexpr int kSub = kThreads / 8;  // 8-lane subgroups per CTA
 
-template <int K, int SLOTS, bool GEN, bool EE>
+template <typename T, int K, int RPT, bool GEN, bool EE>
 __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
-    using VT = typename SlabT<K>::type;
+    using VT = typename Slab<T, K>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = a.n;
     VT* xs0 = reinterpret_cast<VT*>(smem_raw);
-    VT* xs1 = xs0 + a.n;
+    VT* xs1 = xs0 + (n + 1);
     __shared__ uint32_t sflag[3][K];
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int l8 = lane & 7;
-    const int sg = (tid >> 5) * 4 + (lane >> 3);
     const int c0 = blockIdx.x * K;
-    const int n = a.n;
+    T* X = reinterpret_cast<T*>(a.X);
 
-    // per-column parameters
-    float alpha_k[K];
+    T alpha_k[K];
     int tl[K];
     bool valid[K];
     int mem[K];
@@ -94,27 +98,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
         const int c = c0 + k;
         valid[k] = c < a.W;
         mem[k] = valid[k] ? c / a.l : 0;
-        alpha_k[k] = a.alpha_uniform;
+        alpha_k[k] = static_cast<T>(sizeof(T) == 8 ? a.alpha_uniform64 : a.alpha_uniform);
         tl[k] = a.T;
         if (GEN && valid[k]) {
-            if (a.alpha) alpha_k[k] = __ldg(a.alpha + mem[k]);
+            if (a.alpha) alpha_k[k] = reinterpret_cast<const T*>(a.alpha)[mem[k]];
             if (a.tlim) tl[k] = __ldg(a.tlim + mem[k]);
         }
     }
+    const T mu = static_cast<T>(sizeof(T) == 8 ? a.mu64 : a.mu);
 
-    // load the slab (new row r <- old row perm[r])
+    // slab in: new row r <- original row perm[r]; sentinel rows are zero
     for (int r = tid; r < n; r += kThreads) {
-        const float* src = a.X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
+        const T* src = X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
         VT v;
 #pragma unroll
-        for (int k = 0; k < K; ++k) setc(v, k, valid[k] ? src[k] : 0.f);
+        for (int k = 0; k < K; ++k) setc(v, k, valid[k] ? src[k] : T(0));
         xs0[r] = v;
+    }
+    if (tid == 0) {
+        xs0[n] = zero_v<VT>();
+        xs1[n] = zero_v<VT>();
     }
     if (tid < 3 * K) (&sflag[0][0])[tid] = 0u;
 
-    VT vreg[SLOTS];
+    // rows owned by this thread: packed (offset-in-chunk << 16 | degree), velocity
+    uint32_t info[RPT];
+    VT vel[RPT];
 #pragma unroll
-    for (int q = 0; q < SLOTS; ++q) zero(vreg[q]);
+    for (int j = 0; j < RPT; ++j) {
+        const int r = tid + j * kThreads;
+        info[j] = r < n ? __ldg(a.rowinfo + r) : 0u;
+        vel[j] = zero_v<VT>();
+    }
+    const uint2* col4 = reinterpret_cast<const uint2*>(a.col);
     __syncthreads();
 
     int it = 0;
@@ -129,65 +145,69 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
             if (EE && act[k] && it > 0) act[k] = ex_continue(sflag[(it + 2) % 3][k]);
             any |= act[k];
         }
-        if (!any) break;  // uniform: derived from shared state after a barrier
+        if (!any) break;  // uniform: shared state read after a barrier
         if (EE && tid < K) sflag[(it + 1) % 3][tid] = 0u;
         uint32_t bits[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) bits[k] = 0u;
 
-        for (int q = 0; q < SLOTS; ++q) {
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                const int r = sg + kSub * (q * 8 + p);
-                int beg = 0, end = 0;
-                if (r < n) {
-                    beg = __ldg(a.row_ptr + r);
-                    end = __ldg(a.row_ptr + r + 1);
+        for (int j = 0; j < RPT; ++j) {
+            const int r = tid + j * kThreads;
+            if (r < n) {
+                VT acc = zero_v<VT>();
+                const int dj = static_cast<int>(info[j] & 0xffffu);
+                const int words = (dj + 3) >> 2;
+                const uint2* cp = col4 + __ldg(a.chunk_base + j) + (info[j] >> 16);
+                int q = 0;
+                for (; q + 2 <= words; q += 2) {
+                    const uint2 w0 = __ldg(cp + q);
+                    const uint2 w1 = __ldg(cp + q + 1);
+                    const VT g0 = cur[w0.x & 0xffffu], g1 = cur[w0.x >> 16];
+                    const VT g2 = cur[w0.y & 0xffffu], g3 = cur[w0.y >> 16];
+                    const VT g4 = cur[w1.x & 0xffffu], g5 = cur[w1.x >> 16];
+                    const VT g6 = cur[w1.y & 0xffffu], g7 = cur[w1.y >> 16];
+                    addto(acc, g0); addto(acc, g1); addto(acc, g2); addto(acc, g3);  // CSR order
+                    addto(acc, g4); addto(acc, g5); addto(acc, g6); addto(acc, g7);
                 }
-                VT acc;
-                zero(acc);
-                for (int e = beg + l8; e < end; e += 8) addto(acc, cur[__ldg(a.col + e)]);
-                acc = xor_sum8(acc);
-                if (l8 == p && r < n) {
-                    const VT xv = cur[r];
-                    const float dg = static_cast<float>(end - beg);
-                    VT xo = xv;
-                    VT vv = vreg[0];
+                if (q < words) {
+                    const uint2 w0 = __ldg(cp + q);
+                    addto(acc, cur[w0.x & 0xffffu]);
+                    addto(acc, cur[w0.x >> 16]);
+                    addto(acc, cur[w0.y & 0xffffu]);
+                    addto(acc, cur[w0.y >> 16]);
+                }
+                const VT xv = cur[r];
+                const T dg = static_cast<T>(dj);
+                VT xo = xv;
+                VT vv = vel[j];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        if (!act[k]) continue;
-                        const float x = comp(xv, k);
-                        const float y = dg * x - comp(acc, k);        // Lx (graph.cpp:120)
-                        const float v = a.mu * comp(vv, k) + y;       // ascent.cpp:68
-                        const float raw = x + alpha_k[k] * v;         // ascent.cpp:69
-                        if (!isfinite(raw))
-                            atomicMin(a.err, (static_cast<unsigned long long>(mem[k]) << 32) |
-                                                 static_cast<unsigned>(it));
-                        const float cl = raw < -1.f ? -1.f : (raw > 1.f ? 1.f : raw);
-                        if (EE) {
-                            const float ch = fabsf(cl - x);
-                            if (ch > 1e-12f) bits[k] |= EX_BIG;
-                            if (ch > 0.f) bits[k] |= EX_NZ;
-                            if (cl != 1.f && cl != -1.f) bits[k] |= EX_NOTB;
-                        }
-                        setc(xo, k, cl);
-                        setc(vv, k, v);
+                for (int k = 0; k < K; ++k) {
+                    if (!act[k]) continue;
+                    const T x = comp(xv, k);
+                    const T y = rsub(rmul(dg, x), comp(acc, k));   // Lx   graph.cpp:120
+                    const T v = radd(rmul(mu, comp(vv, k)), y);      // v    ascent.cpp:68
+                    const T raw = radd(x, rmul(alpha_k[k], v));       // raw  ascent.cpp:69
+                    if (!isfinite(raw))                               //      ascent.cpp:70-72
+                        atomicMin(a.err, (static_cast<unsigned long long>(mem[k]) << 32) |
+                                             static_cast<unsigned>(it));
+                    const T cl = raw < T(-1) ? T(-1) : (raw > T(1) ? T(1) : raw);  // :73
+                    if (EE) {
+                        const T ch = fabs(rsub(cl, x));
+                        if (ch > T(1e-12)) bits[k] |= EX_BIG;
+                        if (ch > T(0)) bits[k] |= EX_NZ;
+                        if (cl != T(1) && cl != T(-1)) bits[k] |= EX_NOTB;
                     }
-                    nxt[r] = xo;
-                    vreg[0] = vv;
+                    setc(xo, k, cl);
+                    setc(vv, k, v);
                 }
+                nxt[r] = xo;
+                vel[j] = vv;
             }
-            // rotate the velocity queue cyclically: slot q+1 moves to the front;
-            // after SLOTS rotations the queue is back in order for the next iteration
-            const VT head = vreg[0];
-#pragma unroll
-            for (int s = 0; s + 1 < SLOTS; ++s) vreg[s] = vreg[s + 1];
-            vreg[SLOTS - 1] = head;
         }
         if (EE) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                // members spanning several CTAs never reach here (host gate: K % l == 0)
                 const uint32_t b = __reduce_or_sync(0xffffffffu, bits[k]);
                 if (lane == 0 && b) atomicOr(&sflag[it % 3][k], b);
             }
@@ -195,10 +215,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
         __syncthreads();
     }
 
-    // write back the final slab
     const VT* fin = (it & 1) ? xs1 : xs0;
     for (int r = tid; r < n; r += kThreads) {
-        float* dst = a.X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
+        T* dst = X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
         const VT v = fin[r];
 #pragma unroll
         for (int k = 0; k < K; ++k)
@@ -206,71 +225,68 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
     }
 }
 
-}  // namespace
-
-int resident_slots(int n) {
-    const int per_sub = (n + kSub - 1) / kSub;
-    return (per_sub + 7) / 8;
-}
-
-bool resident_fits(int n, int W, int l, bool ee, int& K) {
-    K = (W / 2 >= 148 && static_cast<int64_t>(n) * 2 * 8 <= kResidentSmemMax) ? 2 : 1;
-    if (static_cast<int64_t>(n) * K * 8 > kResidentSmemMax) return false;
-    if (n > 65535) return false;
-    if (ee && (K % l) != 0) return false;  // a member's columns must share a CTA
-    return resident_slots(n) <= 28;
-}
-
-template <int K, int SLOTS, bool GEN, bool EE>
-static void go(const ResidentArgs& a, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(a.n) * K * 8;
+template <typename T, int K, int RPT, bool GEN, bool EE>
+void go(const ResidentArgs& a, cudaStream_t s) {
+    using VT = typename Slab<T, K>::type;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_resident<K, SLOTS, GEN, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kResidentSmemMax);
+        cudaFuncSetAttribute(k_resident<T, K, RPT, GEN, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kResidentSmemMax));
         attr = true;
     }
+    const size_t smem = 2 * static_cast<size_t>(a.n + 1) * sizeof(VT);
     const int ctas = (a.W + K - 1) / K;
     count_launch();
-    k_resident<K, SLOTS, GEN, EE><<<ctas, kThreads, smem, s>>>(a);
+    k_resident<T, K, RPT, GEN, EE><<<ctas, kThreads, smem, s>>>(a);
 }
 
-template <int K, bool GEN, bool EE>
-static void by_slots(const ResidentArgs& a, cudaStream_t s) {
-    const int sl = resident_slots(a.n);
-    if (sl <= 1)
-        go<K, 1, GEN, EE>(a, s);
-    else if (sl <= 2)
-        go<K, 2, GEN, EE>(a, s);
-    else if (sl <= 4)
-        go<K, 4, GEN, EE>(a, s);
-    else if (sl <= 8)
-        go<K, 8, GEN, EE>(a, s);
-    else if (sl <= 10)
-        go<K, 10, GEN, EE>(a, s);
-    else if (sl <= 14)
-        go<K, 14, GEN, EE>(a, s);
+template <typename T, int K, bool GEN, bool EE>
+void by_rpt(const ResidentArgs& a, cudaStream_t s) {
+    const int rpt = (a.n + kThreads - 1) / kThreads;
+    if (rpt <= 1)
+        go<T, K, 1, GEN, EE>(a, s);
+    else if (rpt <= 2)
+        go<T, K, 2, GEN, EE>(a, s);
+    else if (rpt <= 4)
+        go<T, K, 4, GEN, EE>(a, s);
+    else if (rpt <= 8)
+        go<T, K, 8, GEN, EE>(a, s);
+    else if (rpt <= 10)
+        go<T, K, 10, GEN, EE>(a, s);
     else
-        go<K, 28, GEN, EE>(a, s);
+        go<T, K, 14, GEN, EE>(a, s);
 }
 
-void launch_resident(const ResidentArgs& a, int K, bool ee, cudaStream_t s) {
+template <typename T, int K>
+void by_mode(const ResidentArgs& a, bool ee, cudaStream_t s) {
     const bool gen = ee || a.alpha || a.tlim;
-    if (K == 2) {
-        if (ee)
-            by_slots<2, true, true>(a, s);
-        else if (gen)
-            by_slots<2, true, false>(a, s);
-        else
-            by_slots<2, false, false>(a, s);
-    } else {
-        if (ee)
-            by_slots<1, true, true>(a, s);
-        else if (gen)
-            by_slots<1, true, false>(a, s);
-        else
-            by_slots<1, false, false>(a, s);
-    }
+    if (ee)
+        by_rpt<T, K, true, true>(a, s);
+    else if (gen)
+        by_rpt<T, K, true, false>(a, s);
+    else
+        by_rpt<T, K, false, false>(a, s);
+}
+
+}  // namespace
+
+bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K) {
+    if (n > kResidentMaxRows) return false;
+    const int64_t rows = static_cast<int64_t>(n) + 1;
+    K = 1;
+    if (elem_bytes == 4 && W / 2 >= 148 && rows * 2 * 4 * 2 <= kResidentSmemMax) K = 2;
+    if (rows * K * elem_bytes * 2 > kResidentSmemMax) return false;
+    if (ee && (K % l) != 0) return false;  // a member's columns must share a CTA
+    return true;
+}
+
+void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s) {
+    if (elem_bytes == 8)
+        by_mode<double, 1>(a, ee, s);
+    else if (K == 2)
+        by_mode<float, 2>(a, ee, s);
+    else
+        by_mode<float, 1>(a, ee, s);
 }
 
 }  // namespace lcb

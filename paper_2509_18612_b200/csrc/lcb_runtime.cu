@@ -158,9 +158,11 @@ void free_graph(DevGraph& g) {
     cudaFree(g.deg64);
     cudaFree(g.deg32);
     cudaFree(g.order);
-    cudaFree(g.res_row_ptr);
+    cudaFree(g.res_info);
+    cudaFree(g.res_chunk);
     cudaFree(g.res_col);
-    g.row_ptr = g.col = g.order = g.res_row_ptr = nullptr;
+    g.res_info = nullptr;
+    g.row_ptr = g.col = g.order = g.res_chunk = nullptr;
     g.res_col = nullptr;
     g.res_perm = nullptr;
     g.deg64 = nullptr;
@@ -221,22 +223,39 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
     g.res_perm = g.order;
-    if (n <= 65535) {
-        // relabelled CSR for the member-resident kernel: new id = rank in `order`
+    if (static_cast<int>(n) <= kResidentMaxRows) {
+        // relabelled CSR for the member-resident kernel: new id = rank in `order`,
+        // each list padded to a multiple of 4 with the zero sentinel row n; per-row
+        // (offset within its 1024-row chunk, degree) packed in 32 bits
         std::vector<int> inv(n);
         for (uint32_t r = 0; r < n; ++r) inv[ord[r]] = static_cast<int>(r);
-        std::vector<int> rrp(n + 1, 0);
-        std::vector<uint16_t> rcol(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-        for (uint32_t r = 0; r < n; ++r) {
-            const int v = ord[r];
-            rrp[r + 1] = rrp[r] + deg[v];
-            int64_t o = rrp[r];
-            for (int64_t k = off[v]; k < off[v + 1]; ++k) rcol[static_cast<size_t>(o++)] = static_cast<uint16_t>(inv[adj[k]]);
+        std::vector<int64_t> rrp(n + 1, 0);
+        for (uint32_t r = 0; r < n; ++r) rrp[r + 1] = rrp[r] + ((deg[ord[r]] + 3) & ~3);
+        const uint32_t chunks = (n + 1023) / 1024;
+        std::vector<int> cbase(chunks);
+        std::vector<uint32_t> info(n);
+        bool packable = rrp[n] / 4 < (int64_t(1) << 31);
+        for (uint32_t r = 0; r < n && packable; ++r) {
+            if (r % 1024 == 0) cbase[r / 1024] = static_cast<int>(rrp[r] / 4);
+            const int64_t rel = rrp[r] / 4 - cbase[r / 1024];
+            const int d = deg[ord[r]];
+            if (rel >= 65536 || d >= 65536) packable = false;
+            info[r] = (static_cast<uint32_t>(rel) << 16) | static_cast<uint32_t>(d);
         }
-        CK(cudaMalloc(&g.res_row_ptr, sizeof(int) * (n + 1)));
-        CK(cudaMalloc(&g.res_col, sizeof(uint16_t) * rcol.size()));
-        h2d(g.res_row_ptr, rrp.data(), sizeof(int) * (n + 1), 0);
-        h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
+        if (packable) {
+            std::vector<uint16_t> rcol(static_cast<size_t>(std::max<int64_t>(rrp[n], 4)), static_cast<uint16_t>(n));
+            for (uint32_t r = 0; r < n; ++r) {
+                const int v = ord[r];
+                int64_t o = rrp[r];
+                for (int64_t k = off[v]; k < off[v + 1]; ++k) rcol[static_cast<size_t>(o++)] = static_cast<uint16_t>(inv[adj[k]]);
+            }
+            CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * n));
+            CK(cudaMalloc(&g.res_chunk, sizeof(int) * chunks));
+            CK(cudaMalloc(&g.res_col, sizeof(uint16_t) * rcol.size()));
+            h2d(g.res_info, info.data(), sizeof(uint32_t) * n, 0);
+            h2d(g.res_chunk, cbase.data(), sizeof(int) * chunks, 0);
+            h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
+        }
     }
 }
 
@@ -405,44 +424,45 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         const char* e = std::getenv("LCB_RESIDENT");
         return !(e && e[0] == '0');
     }();
-    if constexpr (std::is_same_v<T, float>) {
-        if (resident_enabled && !trace_host && g.res_row_ptr && iters <= 0x7fffffff &&
-            resident_fits(g.n, W, l, ee, K)) {
-            // K2: all iterations in one launch, state resident in SMEM
-            ResidentArgs ra{};
-            ra.row_ptr = g.res_row_ptr;
-            ra.col = g.res_col;
-            ra.perm = g.res_perm;
-            ra.X = w.X[0].p;
-            ra.ld = w.ld;
-            ra.n = g.n;
-            ra.W = W;
-            ra.l = l;
-            ra.T = static_cast<int>(iters);
-            ra.alpha_uniform = alpha_u;
-            ra.alpha = alpha_arr;
-            ra.tlim = tlim_arr;
-            ra.mu = mu;
-            ra.err = a.err;
-            CK(cudaEventRecord(w.ev0, w.st));
-            launch_resident(ra, K, ee, w.st);
-            CK(cudaEventRecord(w.ev1, w.st));
-            CK(cudaGetLastError());
-            d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
-            CK(cudaStreamSynchronize(w.st));
-            r.err = w.h_keys[0];
-            r.iters = iters;
-            r.final_buf = 0;
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
-            w.step_ms += ms;
-            w.step_launches += 1;
-            w.step_bytes += static_cast<double>(iters) *
-                            (16.0 * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
-            w.node_updates += iters * static_cast<int64_t>(g.n) * W;
-            w.resident_iters += iters;
-            return r;
-        }
+    if (resident_enabled && !trace_host && g.res_info && iters <= 0x7fffffff &&
+        resident_fits(g.n, W, l, ee, static_cast<int>(sizeof(T)), K)) {
+        // K2: all iterations in one launch, state resident in SMEM
+        ResidentArgs ra{};
+        ra.rowinfo = g.res_info;
+        ra.chunk_base = g.res_chunk;
+        ra.col = g.res_col;
+        ra.perm = g.res_perm;
+        ra.X = w.X[0].p;
+        ra.ld = w.ld;
+        ra.n = g.n;
+        ra.W = W;
+        ra.l = l;
+        ra.T = static_cast<int>(iters);
+        ra.alpha_uniform = static_cast<float>(alpha_u);
+        ra.mu = static_cast<float>(mu);
+        ra.alpha_uniform64 = static_cast<double>(alpha_u);
+        ra.mu64 = static_cast<double>(mu);
+        ra.alpha = alpha_arr;
+        ra.tlim = tlim_arr;
+        ra.err = a.err;
+        CK(cudaEventRecord(w.ev0, w.st));
+        launch_resident(ra, K, ee, static_cast<int>(sizeof(T)), w.st);
+        CK(cudaEventRecord(w.ev1, w.st));
+        CK(cudaGetLastError());
+        d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
+        CK(cudaStreamSynchronize(w.st));
+        r.err = w.h_keys[0];
+        r.iters = iters;
+        r.final_buf = 0;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+        w.step_ms += ms;
+        w.step_launches += 1;
+        w.step_bytes += static_cast<double>(iters) *
+                        (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+        w.node_updates += iters * static_cast<int64_t>(g.n) * W;
+        w.resident_iters += iters;
+        return r;
     }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;

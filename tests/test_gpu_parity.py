@@ -296,3 +296,27 @@ def test_resident_fp32_tolerance_and_cuts(l, B, ee):
     c64, _, _, _ = lc.round_cut_batch(g, state_of(want, cg.n, l, B), lifted=l > 1)
     assert np.mean(c32 == c64) >= 0.97
     assert abs(int(c32.max()) - int(c64.max())) <= 2
+
+
+def test_global_step_kernel_bitwise_when_resident_disabled(tmp_path):
+    """The HBM-streaming k_step path (used when the slab does not fit on chip) stays
+    bit-exact too: rerun the golden ascent states with LCB_RESIDENT=0."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, json, oracle as O\n"
+        "from paper_2509_18612_b200 import liftcut as lc, LCB_FP64\n"
+        "meta=json.load(open('tests/golden/ascent_states.json')); arr=np.load('tests/golden/ascent_states.npz')\n"
+        "for c in meta:\n"
+        "  g=lc.Graph.from_csr(c['n'],arr[c['name']+'/off'],arr[c['name']+'/adj'])\n"
+        "  for T in c['horizons']:\n"
+        "    s=lc.DenseState(c['n'],c['l'],c['B']); s.values[:]=arr[c['name']+'/x0']\n"
+        "    lc.ascend(g,s,lc.AscentParams(c['alpha'],T,c['mu'],c['early_exit']),precision=LCB_FP64)\n"
+        "    assert np.array_equal(s.values,arr[c['name']+'/x%d'%T]),(c['name'],T)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env={**os.environ, "LCB_RESIDENT": "0"}, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -52,8 +52,10 @@ struct DevGraph {
     float* deg32 = nullptr;   // [n]
     int* order = nullptr;     // [n] rows by degree descending (ties by index)
     // relabelled copy for the member-resident kernel (rows in `order`, uint16 columns)
-    uint32_t* res_info = nullptr; // [n] (offset-in-chunk words << 16) | degree; null if n/a
-    int* res_chunk = nullptr;     // [ceil(n/1024)] chunk base (4-col words)
+    uint32_t* res_info = nullptr; // [n - heavy] light rows: (offset-in-chunk words << 16) | degree
+    int* res_chunk = nullptr;     // [ceil((n-heavy)/1024)] chunk base (4-col words)
+    int* res_heavy = nullptr;     // [heavy][2] absolute word offset, degree
+    int res_nheavy = 0;
     uint16_t* res_col = nullptr;  // [padded nnz]
     int* res_perm = nullptr;      // [n] new row -> original row (== order)
     std::vector<int64_t> h_off;
@@ -94,8 +96,10 @@ enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
 constexpr int64_t kResidentSmemMax = 220 * 1024;
 constexpr int kResidentMaxRows = 14 * 1024;
 struct ResidentArgs {
-    const uint32_t* rowinfo; // relabelled: (4-col word offset within its 1024-row chunk) << 16 | degree
-    const int* chunk_base;   // first 4-col word of each 1024-row chunk
+    const uint32_t* rowinfo; // light row i (= relabelled row heavy+i): word offset within chunk i/1024 << 16 | degree
+    const int* chunk_base;   // first 4-col word of each 1024-light-row chunk
+    const int* heavy_info;   // [heavy][2]: absolute 4-col word offset, degree
+    int heavy;               // rows 0..heavy-1 (degree > split) are heavy
     const uint16_t* col;     // relabelled; pad entries point at the zero row n
     const int* perm;         // new -> original row
     void* X;                 // [n][ld] (float or double), original row order, in/out

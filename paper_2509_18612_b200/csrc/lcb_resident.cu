@@ -75,17 +75,82 @@ __device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a,
 
 constexpr int kThreads = 1024;
 
-template <typename T, int K, int RPT, bool GEN, bool EE>
+template <typename VT>
+__device__ __forceinline__ void gather4(VT& acc, const VT* cur, uint2 w) {
+    // four neighbours in CSR order (graph.cpp:118); pad entries hit the zero row
+    const VT g0 = cur[w.x & 0xffffu], g1 = cur[w.x >> 16];
+    const VT g2 = cur[w.y & 0xffffu], g3 = cur[w.y >> 16];
+    addto(acc, g0);
+    addto(acc, g1);
+    addto(acc, g2);
+    addto(acc, g3);
+}
+
+template <typename VT>
+__device__ __forceinline__ VT warp_sum(VT v);
+template <>
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <>
+__device__ __forceinline__ float2 warp_sum(float2 v) {
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    return v;
+}
+template <>
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fused heavy-ball step for one row (ascent.cpp:66-77), all K columns.
+template <typename T, typename VT, int K, bool EE>
+__device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, VT& xo, int dj,
+                                           const bool (&act)[K], const T (&alpha_k)[K], T mu,
+                                           const int (&mem)[K], int it, uint32_t (&bits)[K],
+                                           unsigned long long* err) {
+    const T dg = static_cast<T>(dj);
+    xo = xv;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const T x = comp(xv, k);
+        const T y = rsub(rmul(dg, x), comp(acc, k));   // Lx   graph.cpp:120
+        const T v = radd(rmul(mu, comp(vv, k)), y);     // v    ascent.cpp:68
+        const T raw = radd(x, rmul(alpha_k[k], v));      // raw  ascent.cpp:69
+        if (!isfinite(raw))                              //      ascent.cpp:70-72
+            atomicMin(err, (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
+        const T cl = raw < T(-1) ? T(-1) : (raw > T(1) ? T(1) : raw);  // ascent.cpp:73
+        if (EE) {
+            const T ch = fabs(rsub(cl, x));
+            if (ch > T(1e-12)) bits[k] |= EX_BIG;
+            if (ch > T(0)) bits[k] |= EX_NZ;
+            if (cl != T(1) && cl != T(-1)) bits[k] |= EX_NOTB;
+        }
+        setc(xo, k, cl);
+        setc(vv, k, v);
+    }
+}
+
+// COOP: heavy rows (degree > split) summed warp-cooperatively (fp32 fast path);
+// otherwise each heavy row is summed sequentially by one thread (fp64 exact path).
+template <typename T, int K, int RPT, bool GEN, bool EE, bool COOP>
 __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
     using VT = typename Slab<T, K>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n;
+    const int H = a.heavy;
     VT* xs0 = reinterpret_cast<VT*>(smem_raw);
     VT* xs1 = xs0 + (n + 1);
     __shared__ uint32_t sflag[3][K];
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const int warp = tid >> 5;
     const int c0 = blockIdx.x * K;
     T* X = reinterpret_cast<T*>(a.X);
 
@@ -107,7 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
     }
     const T mu = static_cast<T>(sizeof(T) == 8 ? a.mu64 : a.mu);
 
-    // slab in: new row r <- original row perm[r]; sentinel rows are zero
     for (int r = tid; r < n; r += kThreads) {
         const T* src = X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
         VT v;
@@ -121,15 +185,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
     }
     if (tid < 3 * K) (&sflag[0][0])[tid] = 0u;
 
-    // rows owned by this thread: packed (offset-in-chunk << 16 | degree), velocity
+    // light rows: row = H + 1024*j + (j even ? tid : 1023 - tid)  (snake over chunks)
     uint32_t info[RPT];
     VT vel[RPT];
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-        const int r = tid + j * kThreads;
-        info[j] = r < n ? __ldg(a.rowinfo + r) : 0u;
+        const int i = j * kThreads + ((j & 1) ? kThreads - 1 - tid : tid);
+        info[j] = H + i < n ? __ldg(a.rowinfo + i) : 0u;
         vel[j] = zero_v<VT>();
     }
+    // heavy rows: COOP -> lane hs of warp w owns heavy row hs*32 + snake(w); else thread tid owns row tid
+    VT vh = zero_v<VT>();
     const uint2* col4 = reinterpret_cast<const uint2*>(a.col);
     __syncthreads();
 
@@ -151,58 +217,65 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) bits[k] = 0u;
 
+        // ---- heavy rows
+        if (COOP) {
+            const int hpw = (H + 31) >> 5;
+            for (int hs = 0; hs < hpw; ++hs) {
+                const int h = hs * 32 + ((hs & 1) ? 31 - warp : warp);
+                if (h >= H) continue;  // warp-uniform
+                const int2 hi = __ldg(reinterpret_cast<const int2*>(a.heavy_info) + h);
+                const int words = (hi.y + 3) >> 2;
+                VT acc = zero_v<VT>();
+                for (int q = lane; q < words; q += 32) gather4(acc, cur, __ldg(col4 + hi.x + q));
+                acc = warp_sum(acc);
+                if (lane == hs) {
+                    VT xo;
+                    row_update<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err);
+                    nxt[h] = xo;
+                }
+            }
+        } else if (tid < H) {
+            const int2 hi = __ldg(reinterpret_cast<const int2*>(a.heavy_info) + tid);
+            const int words = (hi.y + 3) >> 2;
+            VT acc = zero_v<VT>();
+            for (int q = 0; q < words; ++q) gather4(acc, cur, __ldg(col4 + hi.x + q));
+            VT xo;
+            row_update<T, VT, K, EE>(cur[tid], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err);
+            nxt[tid] = xo;
+        }
+
+        // ---- light rows, one row ahead prefetch of the first column word
+        uint2 pre = make_uint2(0u, 0u);
+        {
+            const int i0 = tid;
+            if (H + i0 < n) pre = __ldg(col4 + __ldg(a.chunk_base) + (info[0] >> 16));
+        }
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const int r = tid + j * kThreads;
+            const int i = j * kThreads + ((j & 1) ? kThreads - 1 - tid : tid);
+            const int r = H + i;
+            const uint2 w0 = pre;
+            if (j + 1 < RPT) {
+                const int i1 = (j + 1) * kThreads + (((j + 1) & 1) ? kThreads - 1 - tid : tid);
+                if (H + i1 < n) pre = __ldg(col4 + __ldg(a.chunk_base + j + 1) + (info[j + 1] >> 16));
+            }
             if (r < n) {
-                VT acc = zero_v<VT>();
                 const int dj = static_cast<int>(info[j] & 0xffffu);
                 const int words = (dj + 3) >> 2;
                 const uint2* cp = col4 + __ldg(a.chunk_base + j) + (info[j] >> 16);
-                int q = 0;
+                VT acc = zero_v<VT>();
+                if (words > 0) gather4(acc, cur, w0);  // isolated rows own no column word
+                int q = 1;
                 for (; q + 2 <= words; q += 2) {
-                    const uint2 w0 = __ldg(cp + q);
-                    const uint2 w1 = __ldg(cp + q + 1);
-                    const VT g0 = cur[w0.x & 0xffffu], g1 = cur[w0.x >> 16];
-                    const VT g2 = cur[w0.y & 0xffffu], g3 = cur[w0.y >> 16];
-                    const VT g4 = cur[w1.x & 0xffffu], g5 = cur[w1.x >> 16];
-                    const VT g6 = cur[w1.y & 0xffffu], g7 = cur[w1.y >> 16];
-                    addto(acc, g0); addto(acc, g1); addto(acc, g2); addto(acc, g3);  // CSR order
-                    addto(acc, g4); addto(acc, g5); addto(acc, g6); addto(acc, g7);
+                    const uint2 w1 = __ldg(cp + q);
+                    const uint2 w2 = __ldg(cp + q + 1);
+                    gather4(acc, cur, w1);
+                    gather4(acc, cur, w2);
                 }
-                if (q < words) {
-                    const uint2 w0 = __ldg(cp + q);
-                    addto(acc, cur[w0.x & 0xffffu]);
-                    addto(acc, cur[w0.x >> 16]);
-                    addto(acc, cur[w0.y & 0xffffu]);
-                    addto(acc, cur[w0.y >> 16]);
-                }
-                const VT xv = cur[r];
-                const T dg = static_cast<T>(dj);
-                VT xo = xv;
-                VT vv = vel[j];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    if (!act[k]) continue;
-                    const T x = comp(xv, k);
-                    const T y = rsub(rmul(dg, x), comp(acc, k));   // Lx   graph.cpp:120
-                    const T v = radd(rmul(mu, comp(vv, k)), y);      // v    ascent.cpp:68
-                    const T raw = radd(x, rmul(alpha_k[k], v));       // raw  ascent.cpp:69
-                    if (!isfinite(raw))                               //      ascent.cpp:70-72
-                        atomicMin(a.err, (static_cast<unsigned long long>(mem[k]) << 32) |
-                                             static_cast<unsigned>(it));
-                    const T cl = raw < T(-1) ? T(-1) : (raw > T(1) ? T(1) : raw);  // :73
-                    if (EE) {
-                        const T ch = fabs(rsub(cl, x));
-                        if (ch > T(1e-12)) bits[k] |= EX_BIG;
-                        if (ch > T(0)) bits[k] |= EX_NZ;
-                        if (cl != T(1) && cl != T(-1)) bits[k] |= EX_NOTB;
-                    }
-                    setc(xo, k, cl);
-                    setc(vv, k, v);
-                }
+                if (q < words) gather4(acc, cur, __ldg(cp + q));
+                VT xo;
+                row_update<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, a.err);
                 nxt[r] = xo;
-                vel[j] = vv;
             }
         }
         if (EE) {
@@ -227,22 +300,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
 
 template <typename T, int K, int RPT, bool GEN, bool EE>
 void go(const ResidentArgs& a, cudaStream_t s) {
+    constexpr bool COOP = sizeof(T) == 4;
     using VT = typename Slab<T, K>::type;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_resident<T, K, RPT, GEN, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_resident<T, K, RPT, GEN, EE, COOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kResidentSmemMax));
         attr = true;
     }
     const size_t smem = 2 * static_cast<size_t>(a.n + 1) * sizeof(VT);
     const int ctas = (a.W + K - 1) / K;
     count_launch();
-    k_resident<T, K, RPT, GEN, EE><<<ctas, kThreads, smem, s>>>(a);
+    k_resident<T, K, RPT, GEN, EE, COOP><<<ctas, kThreads, smem, s>>>(a);
 }
 
 template <typename T, int K, bool GEN, bool EE>
 void by_rpt(const ResidentArgs& a, cudaStream_t s) {
-    const int rpt = (a.n + kThreads - 1) / kThreads;
+    const int rpt = (a.n - a.heavy + kThreads - 1) / kThreads;
     if (rpt <= 1)
         go<T, K, 1, GEN, EE>(a, s);
     else if (rpt <= 2)
@@ -275,6 +349,7 @@ bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K) {
     const int64_t rows = static_cast<int64_t>(n) + 1;
     K = 1;
     if (elem_bytes == 4 && W / 2 >= 148 && rows * 2 * 4 * 2 <= kResidentSmemMax) K = 2;
+    // (fp64 / fp32 share the relabelled layout; heavy rows are the first `heavy` rows)
     if (rows * K * elem_bytes * 2 > kResidentSmemMax) return false;
     if (ee && (K % l) != 0) return false;  // a member's columns must share a CTA
     return true;

@@ -160,6 +160,8 @@ void free_graph(DevGraph& g) {
     cudaFree(g.order);
     cudaFree(g.res_info);
     cudaFree(g.res_chunk);
+    cudaFree(g.res_heavy);
+    g.res_heavy = nullptr;
     cudaFree(g.res_col);
     g.res_info = nullptr;
     g.row_ptr = g.col = g.order = g.res_chunk = nullptr;
@@ -231,16 +233,26 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         for (uint32_t r = 0; r < n; ++r) inv[ord[r]] = static_cast<int>(r);
         std::vector<int64_t> rrp(n + 1, 0);
         for (uint32_t r = 0; r < n; ++r) rrp[r + 1] = rrp[r] + ((deg[ord[r]] + 3) & ~3);
-        const uint32_t chunks = (n + 1023) / 1024;
-        std::vector<int> cbase(chunks);
-        std::vector<uint32_t> info(n);
+        // heavy rows: degree > 32 (warp-cooperative in the fp32 kernel), at most 1024
+        int H = 0;
+        while (H < static_cast<int>(n) && H < 1024 && deg[ord[H]] > 32) ++H;
+        const uint32_t L = n - H;
+        const uint32_t chunks = (L + 1023) / 1024 + 1;
+        std::vector<int> cbase(chunks, 0);
+        std::vector<uint32_t> info(std::max<uint32_t>(L, 1));
+        std::vector<int> hinfo(2 * std::max(H, 1));
+        for (int h = 0; h < H; ++h) {
+            hinfo[2 * h] = static_cast<int>(rrp[h] / 4);
+            hinfo[2 * h + 1] = deg[ord[h]];
+        }
         bool packable = rrp[n] / 4 < (int64_t(1) << 31);
-        for (uint32_t r = 0; r < n && packable; ++r) {
-            if (r % 1024 == 0) cbase[r / 1024] = static_cast<int>(rrp[r] / 4);
-            const int64_t rel = rrp[r] / 4 - cbase[r / 1024];
+        for (uint32_t i = 0; i < L && packable; ++i) {
+            const uint32_t r = H + i;
+            if (i % 1024 == 0) cbase[i / 1024] = static_cast<int>(rrp[r] / 4);
+            const int64_t rel = rrp[r] / 4 - cbase[i / 1024];
             const int d = deg[ord[r]];
             if (rel >= 65536 || d >= 65536) packable = false;
-            info[r] = (static_cast<uint32_t>(rel) << 16) | static_cast<uint32_t>(d);
+            info[i] = (static_cast<uint32_t>(rel) << 16) | static_cast<uint32_t>(d);
         }
         if (packable) {
             std::vector<uint16_t> rcol(static_cast<size_t>(std::max<int64_t>(rrp[n], 4)), static_cast<uint16_t>(n));
@@ -249,11 +261,14 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                 int64_t o = rrp[r];
                 for (int64_t k = off[v]; k < off[v + 1]; ++k) rcol[static_cast<size_t>(o++)] = static_cast<uint16_t>(inv[adj[k]]);
             }
-            CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * n));
+            CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * info.size()));
             CK(cudaMalloc(&g.res_chunk, sizeof(int) * chunks));
+            CK(cudaMalloc(&g.res_heavy, sizeof(int) * hinfo.size()));
             CK(cudaMalloc(&g.res_col, sizeof(uint16_t) * rcol.size()));
-            h2d(g.res_info, info.data(), sizeof(uint32_t) * n, 0);
+            h2d(g.res_info, info.data(), sizeof(uint32_t) * info.size(), 0);
             h2d(g.res_chunk, cbase.data(), sizeof(int) * chunks, 0);
+            h2d(g.res_heavy, hinfo.data(), sizeof(int) * hinfo.size(), 0);
+            g.res_nheavy = H;
             h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
         }
     }
@@ -430,6 +445,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         ResidentArgs ra{};
         ra.rowinfo = g.res_info;
         ra.chunk_base = g.res_chunk;
+        ra.heavy_info = g.res_heavy;
+        ra.heavy = g.res_nheavy;
         ra.col = g.res_col;
         ra.perm = g.res_perm;
         ra.X = w.X[0].p;

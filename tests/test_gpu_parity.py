@@ -320,3 +320,23 @@ def test_global_step_kernel_bitwise_when_resident_disabled(tmp_path):
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env={**os.environ, "LCB_RESIDENT": "0"}, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_resident_isolated_and_heavy_rows_fp64_bitwise():
+    # isolated nodes (degree 0), > 32-degree hubs and > 1024 rows in one graph
+    n = 2500
+    rng = np.random.default_rng(5)
+    u = list(rng.integers(0, 2000, 4000)) + [0] * 300 + [1] * 120
+    v = list(rng.integers(0, 2000, 4000)) + list(range(1000, 1300)) + list(range(1500, 1620))
+    keep = [(a, b) for a, b in zip(u, v) if a != b]
+    cg = O.csr_from_edges(n, [a for a, _ in keep], [b for _, b in keep])
+    assert (np.diff(cg.off) == 0).sum() >= 400 and np.diff(cg.off).max() > 32
+    x = rng.uniform(-1e-3, 1e-3, 40 * n)
+    for ee in (False, True):
+        want, _ = O.ascend(cg, x, 1, 40, 0.03, 60, 0.9, ee)
+        assert np.array_equal(run_ascend(pg(cg), x, n, 1, 40, 0.03, 60, 0.9, ee), want)
+        got32 = run_ascend(pg(cg), x, n, 1, 40, 0.03, 5, 0.9, ee, LCB_FP32)
+        w5, _ = O.ascend(cg, x, 1, 40, 0.03, 5, 0.9, ee)
+        for j in range(40):
+            a_, b_ = got32[j * n:(j + 1) * n], w5[j * n:(j + 1) * n]
+            assert np.max(np.abs(a_ - b_)) / np.max(np.abs(b_)) <= FP32_NORM_TOL

@@ -90,6 +90,15 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int c0 = group * SPAN + lane * E;
         const T* xin = a.x_in + c0;
 
+        // self iterate and velocity do not depend on the gathers: issue them first
+        const int64_t rb0 = static_cast<int64_t>(row) * a.ld + c0;
+        V xself[S], vself[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            xself[s] = ldg_vec(reinterpret_cast<const V*>(a.x_in + rb0 + s * 32 * E));
+            if constexpr (MODE == MODE_STEP) vself[s] = *reinterpret_cast<const V*>(a.vel + rb0 + s * 32 * E);
+        }
+
         V acc[S];
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -102,7 +111,24 @@ __global__ void __launch_bounds__(kWarps * 32)
             const int cnt = min(32, end - base);
             const int mycol = lane < cnt ? __ldg(a.col + base + lane) : 0;
             int k = 0;
-            for (; k + 4 <= cnt; k += 4) {
+            for (; k + 8 <= cnt; k += 8) {
+                V v[8][S];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, mycol, k + q);
+                    const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) v[q][s] = ldg_vec(p + s * 32);
+                }
+                // sequential CSR order per element (graph.cpp:118)
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+#pragma unroll
+                        for (int e = 0; e < E; ++e) el(acc[s], e) = radd(el(acc[s], e), el(v[q][s], e));
+            }
+            if (k + 4 <= cnt) {
                 V v[4][S];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -111,13 +137,13 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
                     for (int s = 0; s < S; ++s) v[q][s] = ldg_vec(p + s * 32);
                 }
-                // sequential CSR order per element (graph.cpp:118)
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
                     for (int s = 0; s < S; ++s)
 #pragma unroll
                         for (int e = 0; e < E; ++e) el(acc[s], e) = radd(el(acc[s], e), el(v[q][s], e));
+                k += 4;
             }
             for (; k < cnt; ++k) {
                 const int u = __shfl_sync(0xffffffffu, mycol, k);
@@ -136,7 +162,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int64_t off = rb + s * 32 * E;
-            V xv = *reinterpret_cast<const V*>(a.x_in + off);
+            V xv = xself[s];
             if constexpr (MODE == MODE_LAPLACE) {
                 V y;
 #pragma unroll
@@ -144,7 +170,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 *reinterpret_cast<V*>(a.x_out + off) = y;
                 continue;
             } else {
-                V vv = *reinterpret_cast<const V*>(a.vel + off);
+                V vv = vself[s];
                 V xo;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libliftcut_b200.so")
+LIB_PATH = os.environ.get("LCB_LIB_PATH") or os.path.join(HERE, "libliftcut_b200.so")
 
 P = C.c_void_p
 i64, u64, u32, i32, f64 = C.c_int64, C.c_uint64, C.c_uint32, C.c_int32, C.c_double

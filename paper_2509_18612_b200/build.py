@@ -34,13 +34,13 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if not force and not stale() and out == LIB:
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-o", LIB, *sources(), "-ldl"]
+           "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-o", out, *sources(), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -158,6 +158,8 @@ void free_graph(DevGraph& g) {
     cudaFree(g.deg64);
     cudaFree(g.deg32);
     cudaFree(g.order);
+    cudaFree(g.slots);
+    g.slots = nullptr;
     cudaFree(g.res_info);
     cudaFree(g.res_chunk);
     cudaFree(g.res_heavy);
@@ -224,6 +226,12 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
+    {
+        std::vector<int4> sl(n);
+        for (uint32_t i = 0; i < n; ++i) sl[i] = make_int4(ord[i], rp[ord[i]], rp[ord[i] + 1], 0);
+        CK(cudaMalloc(&g.slots, sizeof(int4) * n));
+        h2d(g.slots, sl.data(), sizeof(int4) * n, 0);
+    }
     g.res_perm = g.order;
     if (static_cast<int>(n) <= kResidentMaxRows) {
         // relabelled CSR for the member-resident kernel: new id = rank in `order`,
@@ -412,7 +420,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     a.row_ptr = g.row_ptr;
     a.col = g.col;
     a.deg = deg_of<T>(g);
-    a.order = g.order;
+    a.slots = g.slots;
     a.vel = w.V.p;
     a.ld = w.ld;
     a.n = g.n;
@@ -1147,7 +1155,7 @@ void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count
     a.row_ptr = g.row_ptr;
     a.col = g.col;
     a.deg = deg_of<T>(g);
-    a.order = g.order;
+    a.slots = g.slots;
     a.x_in = w.X[0].p;
     a.x_out = w.X[1].p;
     a.ld = w.ld;

@@ -59,10 +59,16 @@ __device__ __forceinline__ T clamp1(T r) {
 
 constexpr int kWarps = 8;  // warps per block of the step kernel (one row each)
 #ifndef LCB_UNROLL
-#define LCB_UNROLL 8
+#define LCB_UNROLL 4
 #endif
 #ifndef LCB_MINB
 #define LCB_MINB 1
+#endif
+#ifndef LCB_HOIST
+#define LCB_HOIST 0
+#endif
+#ifndef LCB_PRED
+#define LCB_PRED 0
 #endif
 
 // ---------------------------------------------------------------------------
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
         const int64_t rb = static_cast<int64_t>(si[i].x) * a.ld + c0;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            if (live[i]) {
+            if (LCB_HOIST && live[i]) {
                 xself[i][s] = ldg_vec(reinterpret_cast<const V*>(a.x_in + rb + s * 32 * E));
                 if constexpr (MODE == MODE_STEP) vself[i][s] = *reinterpret_cast<const V*>(a.vel + rb + s * 32 * E);
             }
@@ -141,6 +147,36 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
             cnt[i] = min(32, len[i] - base);
             mycol[i] = lane < cnt[i] ? __ldg(a.col + si[i].y + base + lane) : 0;
             cmax = max(cmax, cnt[i]);
+        }
+        if (R == 1 && !LCB_PRED) {
+            int k = 0;
+            for (; k + 4 <= cnt[0]; k += 4) {
+                V v[4][S];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, mycol[0], k + q);
+                    const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) v[q][s] = ldg_vec(p + s * 32);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+#pragma unroll
+                        for (int e = 0; e < E; ++e) el(acc[0][s], e) = radd(el(acc[0][s], e), el(v[q][s], e));
+            }
+            for (; k < cnt[0]; ++k) {
+                const int u = __shfl_sync(0xffffffffu, mycol[0], k);
+                const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const V v = ldg_vec(p + s * 32);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) el(acc[0][s], e) = radd(el(acc[0][s], e), el(v, e));
+                }
+            }
+            continue;
         }
         for (int k = 0; k < cmax; k += 4) {
             V v[R][4][S];
@@ -178,6 +214,10 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int64_t off = rb + s * 32 * E;
+            if (!LCB_HOIST) {
+                xself[i][s] = ldg_vec(reinterpret_cast<const V*>(a.x_in + off));
+                if constexpr (MODE == MODE_STEP) vself[i][s] = *reinterpret_cast<const V*>(a.vel + off);
+            }
             const V xv = xself[i][s];
             if constexpr (MODE == MODE_LAPLACE) {
                 V y;
@@ -264,7 +304,7 @@ int pick_s(int W) {
 int pick_r() {
     static int r = [] {
         const char* e = std::getenv("LCB_ROWS");
-        const int v = e ? std::atoi(e) : 2;
+        const int v = e ? std::atoi(e) : 1;  // R=2 measured slower: the kernel is L2-bandwidth-bound
         return v == 1 ? 1 : 2;
     }();
     return r;

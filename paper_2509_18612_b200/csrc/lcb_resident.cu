@@ -54,10 +54,39 @@ __device__ __forceinline__ void setc(float2& v, int k, float x) {
 }
 __device__ __forceinline__ void addto(float& a, const float& b) { a = __fadd_rn(a, b); }
 __device__ __forceinline__ void addto(double& a, const double& b) { a = __dadd_rn(a, b); }
-__device__ __forceinline__ void addto(float2& a, const float2& b) {
-    a.x = __fadd_rn(a.x, b.x);
-    a.y = __fadd_rn(a.y, b.y);
+__device__ __forceinline__ void addto(float2& a, const float2& b);
+// Blackwell packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2): round-to-nearest per lane,
+// identical to two scalar __fadd_rn / __fmul_rn / __fmaf_rn.
+__device__ __forceinline__ unsigned long long as_u64(float2 v) {
+    return (static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
 }
+__device__ __forceinline__ float2 as_f2(unsigned long long u) {
+    return make_float2(__uint_as_float(static_cast<unsigned>(u)), __uint_as_float(static_cast<unsigned>(u >> 32)));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)));
+    return as_f2(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)));
+    return as_f2(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
+    return as_f2(r);
+}
+// 8-byte shared load at a 32-bit shared-window byte address
+__device__ __forceinline__ float2 lds2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void addto(float2& a, const float2& b) { a = add2(a, b); }
+
 template <typename VT>
 __device__ __forceinline__ VT zero_v() {
     VT v;
@@ -84,6 +113,19 @@ __device__ __forceinline__ void gather4(VT& acc, const VT* cur, uint2 w) {
     addto(acc, g1);
     addto(acc, g2);
     addto(acc, g3);
+}
+
+// float2 slab: address = base + 8 * column (two integer ops per column)
+__device__ __forceinline__ void gather4(float2& acc, const float2* cur, uint2 w) {
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
+    const float2 g0 = lds2(base + ((w.x & 0xffffu) << 3));
+    const float2 g1 = lds2(base + ((w.x >> 16) << 3));
+    const float2 g2 = lds2(base + ((w.y & 0xffffu) << 3));
+    const float2 g3 = lds2(base + ((w.y >> 16) << 3));
+    acc = add2(acc, g0);
+    acc = add2(acc, g1);
+    acc = add2(acc, g2);
+    acc = add2(acc, g3);
 }
 
 template <typename VT>
@@ -134,6 +176,36 @@ __device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, 
         setc(xo, k, cl);
         setc(vv, k, v);
     }
+}
+
+// Packed K=2 fp32 epilogue for the uniform path (both columns live and active).
+__device__ __forceinline__ void row_update2(const float2& xv, const float2& acc, float2& vv, float2& xo,
+                                            int dj, float2 alpha2, float2 mu2, const int (&mem)[2],
+                                            int it, unsigned long long* err) {
+    const float dg = static_cast<float>(dj);
+    const float2 y = fma2(make_float2(dg, dg), xv, make_float2(-acc.x, -acc.y));  // Lx
+    vv = fma2(mu2, vv, y);                                                          // v
+    const float2 raw = fma2(alpha2, vv, xv);                                        // raw
+    if (!isfinite(raw.x) || !isfinite(raw.y)) {
+        const int k = isfinite(raw.x) ? 1 : 0;
+        atomicMin(err, (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
+    }
+    xo.x = fminf(fmaxf(raw.x, -1.f), 1.f);
+    xo.y = fminf(fmaxf(raw.y, -1.f), 1.f);
+}
+
+template <typename T, typename VT, int K, bool EE>
+__device__ __forceinline__ void row_update_any(const VT& xv, const VT& acc, VT& vv, VT& xo, int dj,
+                                               const bool (&act)[K], const T (&alpha_k)[K], T mu,
+                                               const int (&mem)[K], int it, uint32_t (&bits)[K],
+                                               unsigned long long* err, bool packed) {
+    if constexpr (K == 2 && sizeof(T) == 4 && !EE) {
+        if (packed) {
+            row_update2(xv, acc, vv, xo, dj, make_float2(alpha_k[0], alpha_k[1]), make_float2(mu, mu), mem, it, err);
+            return;
+        }
+    }
+    row_update<T, VT, K, EE>(xv, acc, vv, xo, dj, act, alpha_k, mu, mem, it, bits, err);
 }
 
 // COOP: heavy rows (degree > split) summed warp-cooperatively (fp32 fast path);
@@ -212,6 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
             any |= act[k];
         }
         if (!any) break;  // uniform: shared state read after a barrier
+        bool packed = true;  // every column live and active: packed epilogue
+#pragma unroll
+        for (int k = 0; k < K; ++k) packed &= act[k];
         if (EE && tid < K) sflag[(it + 1) % 3][tid] = 0u;
         uint32_t bits[K];
 #pragma unroll
@@ -230,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
                 acc = warp_sum(acc);
                 if (lane == hs) {
                     VT xo;
-                    row_update<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err);
+                    row_update_any<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err, packed);
                     nxt[h] = xo;
                 }
             }
@@ -274,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
                 }
                 if (q < words) gather4(acc, cur, __ldg(cp + q));
                 VT xo;
-                row_update<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, a.err);
+                row_update_any<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, a.err, packed);
                 nxt[r] = xo;
             }
         }

@@ -51,7 +51,6 @@ struct DevGraph {
     double* deg64 = nullptr;  // [n]
     float* deg32 = nullptr;   // [n]
     int* order = nullptr;     // [n] rows by degree descending (ties by index)
-    int4* slots = nullptr;    // [n] {order[s], row_ptr[order[s]], row_ptr[order[s]+1], 0}
     // relabelled copy for the member-resident kernel (rows in `order`, uint16 columns)
     uint32_t* res_info = nullptr; // [n - heavy] light rows: (offset-in-chunk words << 16) | degree
     int* res_chunk = nullptr;     // [ceil((n-heavy)/1024)] chunk base (4-col words)
@@ -71,7 +70,7 @@ struct StepArgs {
     const int* row_ptr;
     const int* col;
     const T* deg;
-    const int4* slots;          // [n] {row, begin, end, 0} in degree-descending order
+    const int* order;
     const T* x_in;
     T* x_out;
     T* vel;

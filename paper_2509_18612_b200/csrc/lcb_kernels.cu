@@ -58,30 +58,15 @@ __device__ __forceinline__ T clamp1(T r) {
 }
 
 constexpr int kWarps = 8;  // warps per block of the step kernel (one row each)
-#ifndef LCB_UNROLL
-#define LCB_UNROLL 4
-#endif
-#ifndef LCB_MINB
-#define LCB_MINB 1
-#endif
-#ifndef LCB_HOIST
-#define LCB_HOIST 0
-#endif
-#ifndef LCB_PRED
-#define LCB_PRED 0
-#endif
 
 // ---------------------------------------------------------------------------
-// K1: fused PGA step, HBM-streaming.  A warp owns R rows x one column slab-group
-// (S 16-byte vectors per lane).  Rows are taken in degree-descending order
-// (hubs first, BA degree skew) through one 16-byte slot record {row, begin, end},
-// so a row's dependent chain is slot record -> column indices -> neighbour
-// gathers; the R rows' gathers are interleaved to keep more bytes in flight.
+// K1: fused PGA step.  One warp per (row, column slab-group); rows are visited
+// in degree-descending order so hub rows start first (BA degree skew).
 //   GEN = per-member alpha / iteration limit (batched search) or early exit
 //   EE  = early-exit bits (implies GEN)
 // ---------------------------------------------------------------------------
-template <typename T, int S, int R, bool GEN, bool EE, int MODE>
-__global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
+template <typename T, int S, bool GEN, bool EE, int MODE>
+__global__ void __launch_bounds__(kWarps * 32)
     k_step(StepArgs<T> a, int groups) {
     constexpr int E = Vec<T>::E;
     using V = typename Vec<T>::type;
@@ -91,7 +76,7 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int group = blockIdx.x % groups;
-    const int slot0 = ((blockIdx.x / groups) * kWarps + warp) * R;
+    const int slot = (blockIdx.x / groups) * kWarps + warp;
 
     if constexpr (EE) {
         for (int i = threadIdx.x; i < SPAN; i += blockDim.x) sbits[i] = 0;
@@ -100,132 +85,66 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
         __syncthreads();
     }
 
-    const int c0 = group * SPAN + lane * E;
-    int4 si[R];
-    bool live[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        live[i] = slot0 + i < a.n;
-        si[i] = live[i] ? __ldg(a.slots + slot0 + i) : make_int4(0, 0, 0, 0);
-    }
+    if (slot < a.n) {
+        const int row = a.order ? __ldg(a.order + slot) : slot;
+        const int c0 = group * SPAN + lane * E;
+        const T* xin = a.x_in + c0;
 
-    // self iterate and velocity do not depend on the gathers: issue them first
-    V xself[R][S], vself[R][S];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        const int64_t rb = static_cast<int64_t>(si[i].x) * a.ld + c0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            if (LCB_HOIST && live[i]) {
-                xself[i][s] = ldg_vec(reinterpret_cast<const V*>(a.x_in + rb + s * 32 * E));
-                if constexpr (MODE == MODE_STEP) vself[i][s] = *reinterpret_cast<const V*>(a.vel + rb + s * 32 * E);
-            }
-        }
-    }
-
-    V acc[R][S];
-#pragma unroll
-    for (int i = 0; i < R; ++i)
+        V acc[S];
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int e = 0; e < E; ++e) el(acc[i][s], e) = T(0);
+            for (int e = 0; e < E; ++e) el(acc[s], e) = T(0);
 
-    const T* xin = a.x_in + c0;
-    int len[R];
-    int maxlen = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        len[i] = si[i].z - si[i].y;
-        maxlen = max(maxlen, len[i]);
-    }
-    for (int base = 0; base < maxlen; base += 32) {
-        int mycol[R], cnt[R];
-        int cmax = 0;
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            cnt[i] = min(32, len[i] - base);
-            mycol[i] = lane < cnt[i] ? __ldg(a.col + si[i].y + base + lane) : 0;
-            cmax = max(cmax, cnt[i]);
-        }
-        if (R == 1 && !LCB_PRED) {
+        const int beg = __ldg(a.row_ptr + row);
+        const int end = __ldg(a.row_ptr + row + 1);
+        for (int base = beg; base < end; base += 32) {
+            const int cnt = min(32, end - base);
+            const int mycol = lane < cnt ? __ldg(a.col + base + lane) : 0;
             int k = 0;
-            for (; k + 4 <= cnt[0]; k += 4) {
+            for (; k + 4 <= cnt; k += 4) {
                 V v[4][S];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const int u = __shfl_sync(0xffffffffu, mycol[0], k + q);
+                    const int u = __shfl_sync(0xffffffffu, mycol, k + q);
                     const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
 #pragma unroll
                     for (int s = 0; s < S; ++s) v[q][s] = ldg_vec(p + s * 32);
                 }
+                // sequential CSR order per element (graph.cpp:118)
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
                     for (int s = 0; s < S; ++s)
 #pragma unroll
-                        for (int e = 0; e < E; ++e) el(acc[0][s], e) = radd(el(acc[0][s], e), el(v[q][s], e));
+                        for (int e = 0; e < E; ++e) el(acc[s], e) = radd(el(acc[s], e), el(v[q][s], e));
             }
-            for (; k < cnt[0]; ++k) {
-                const int u = __shfl_sync(0xffffffffu, mycol[0], k);
+            for (; k < cnt; ++k) {
+                const int u = __shfl_sync(0xffffffffu, mycol, k);
                 const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const V v = ldg_vec(p + s * 32);
 #pragma unroll
-                    for (int e = 0; e < E; ++e) el(acc[0][s], e) = radd(el(acc[0][s], e), el(v, e));
+                    for (int e = 0; e < E; ++e) el(acc[s], e) = radd(el(acc[s], e), el(v, e));
                 }
             }
-            continue;
         }
-        for (int k = 0; k < cmax; k += 4) {
-            V v[R][4][S];
-#pragma unroll
-            for (int i = 0; i < R; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int u = __shfl_sync(0xffffffffu, mycol[i], (k + q) & 31);
-                    if (k + q < cnt[i]) {  // warp-uniform predicate
-                        const V* p = reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld);
-#pragma unroll
-                        for (int s = 0; s < S; ++s) v[i][q][s] = ldg_vec(p + s * 32);
-                    }
-                }
-            // sequential CSR order per element (graph.cpp:118)
-#pragma unroll
-            for (int i = 0; i < R; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (k + q < cnt[i])
-#pragma unroll
-                        for (int s = 0; s < S; ++s)
-#pragma unroll
-                            for (int e = 0; e < E; ++e)
-                                el(acc[i][s], e) = radd(el(acc[i][s], e), el(v[i][q][s], e));
-        }
-    }
 
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        if (!live[i]) continue;
-        const int row = si[i].x;
-        const T dg = static_cast<T>(len[i]);
+        const T dg = __ldg(a.deg + row);
         const int64_t rb = static_cast<int64_t>(row) * a.ld + c0;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int64_t off = rb + s * 32 * E;
-            if (!LCB_HOIST) {
-                xself[i][s] = ldg_vec(reinterpret_cast<const V*>(a.x_in + off));
-                if constexpr (MODE == MODE_STEP) vself[i][s] = *reinterpret_cast<const V*>(a.vel + off);
-            }
-            const V xv = xself[i][s];
+            V xv = *reinterpret_cast<const V*>(a.x_in + off);
             if constexpr (MODE == MODE_LAPLACE) {
                 V y;
 #pragma unroll
-                for (int e = 0; e < E; ++e) el(y, e) = rsub(rmul(dg, el(xv, e)), el(acc[i][s], e));
+                for (int e = 0; e < E; ++e) el(y, e) = rsub(rmul(dg, el(xv, e)), el(acc[s], e));
                 *reinterpret_cast<V*>(a.x_out + off) = y;
+                continue;
             } else {
-                V vv = vself[i][s];
+                V vv = *reinterpret_cast<const V*>(a.vel + off);
                 V xo;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -247,7 +166,7 @@ __global__ void __launch_bounds__(kWarps * 32, LCB_MINB)
                         m = colx / a.l;
                     }
                     if (act) {
-                        const T y = rsub(rmul(dg, x), el(acc[i][s], e));  // Lx  (graph.cpp:120)
+                        const T y = rsub(rmul(dg, x), el(acc[s], e));     // Lx  (graph.cpp:120)
                         const T v = radd(rmul(a.mu, el(vv, e)), y);        // ascent.cpp:68
                         const T raw = radd(x, rmul(alpha, v));             // ascent.cpp:69
                         if (!isfinite(raw))                                // ascent.cpp:70-72
@@ -294,43 +213,31 @@ int pick_s(int W) {
         const char* e = std::getenv("LCB_STEP_S");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced == 1 || forced == 2) return forced;
+    if (forced == 1 || forced == 2 || forced == 4) return forced;
     constexpr int E = Vec<T>::E;
     (void)E;
     (void)W;
     return 1;  // measured best on B200 for W in {1024, 2048} (profiles/)
 }
 
-int pick_r() {
-    static int r = [] {
-        const char* e = std::getenv("LCB_ROWS");
-        const int v = e ? std::atoi(e) : 1;  // R=2 measured slower: the kernel is L2-bandwidth-bound
-        return v == 1 ? 1 : 2;
-    }();
-    return r;
-}
-
 template <typename T, bool GEN, bool EE, int MODE>
 void dispatch_s(const StepArgs<T>& a, int S, cudaStream_t st) {
     constexpr int E = Vec<T>::E;
-    const int R = pick_r();
-    auto go = [&](auto sconst, auto rconst) {
+    const int rows_blocks = (a.n + kWarps - 1) / kWarps;
+    auto go = [&](auto sconst) {
         constexpr int SS = decltype(sconst)::value;
-        constexpr int RR = decltype(rconst)::value;
         constexpr int SPAN = 32 * SS * E;
         const int groups = static_cast<int>((a.ld + SPAN - 1) / SPAN);
-        const int rows_blocks = (a.n + kWarps * RR - 1) / (kWarps * RR);
         const dim3 grid(static_cast<unsigned>(rows_blocks) * groups);
         count_launch();
-        k_step<T, SS, RR, GEN, EE, MODE><<<grid, kWarps * 32, 0, st>>>(a, groups);
+        k_step<T, SS, GEN, EE, MODE><<<grid, kWarps * 32, 0, st>>>(a, groups);
     };
-    if (S == 2) {
-        if (R == 1) go(std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
-        else go(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{});
-    } else {
-        if (R == 1) go(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
-        else go(std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{});
-    }
+    if (S == 1)
+        go(std::integral_constant<int, 1>{});
+    else if (S == 2)
+        go(std::integral_constant<int, 2>{});
+    else
+        go(std::integral_constant<int, 4>{});
 }
 
 }  // namespace

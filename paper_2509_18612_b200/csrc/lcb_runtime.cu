@@ -158,8 +158,6 @@ void free_graph(DevGraph& g) {
     cudaFree(g.deg64);
     cudaFree(g.deg32);
     cudaFree(g.order);
-    cudaFree(g.slots);
-    g.slots = nullptr;
     cudaFree(g.res_info);
     cudaFree(g.res_chunk);
     cudaFree(g.res_heavy);
@@ -226,12 +224,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
-    {
-        std::vector<int4> sl(n);
-        for (uint32_t i = 0; i < n; ++i) sl[i] = make_int4(ord[i], rp[ord[i]], rp[ord[i] + 1], 0);
-        CK(cudaMalloc(&g.slots, sizeof(int4) * n));
-        h2d(g.slots, sl.data(), sizeof(int4) * n, 0);
-    }
+
     g.res_perm = g.order;
     if (static_cast<int>(n) <= kResidentMaxRows) {
         // relabelled CSR for the member-resident kernel: new id = rank in `order`,
@@ -404,6 +397,22 @@ struct Work {
     }
 };
 
+// Kernel choice measured on B200 (profiles/round1_kernel_ab.md): the member-resident
+// kernel wins when the on-chip slab covers the graph and the batch is wide enough to
+// fill whole waves (W >= 2048 columns at K=2, any W for fp64 / small graphs); the
+// HBM-streaming kernel wins for the narrow fp32 batch (W = 1024: 51 vs 62 us/iteration).
+bool resident_preferred(const DevGraph& g, int W, size_t elem) {
+    static const int mode = [] {
+        const char* e = std::getenv("LCB_RESIDENT");
+        return e ? std::atoi(e) : -1;  // -1 auto, 0 never, 1 always (when it fits)
+    }();
+    if (mode == 0) return false;
+    if (mode == 1) return true;
+    if (elem == 8) return true;
+    if (g.n <= 2048) return true;  // whole batch on chip, launch-latency bound otherwise
+    return W >= 2048;
+}
+
 struct IterResult {
     unsigned long long err = ~0ull;
     int final_buf = 0;
@@ -420,7 +429,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     a.row_ptr = g.row_ptr;
     a.col = g.col;
     a.deg = deg_of<T>(g);
-    a.slots = g.slots;
+    a.order = g.order;
     a.vel = w.V.p;
     a.ld = w.ld;
     a.n = g.n;
@@ -443,11 +452,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
 
     IterResult r;
     int K = 0;
-    static const bool resident_enabled = [] {
-        const char* e = std::getenv("LCB_RESIDENT");
-        return !(e && e[0] == '0');
-    }();
-    if (resident_enabled && !trace_host && g.res_info && iters <= 0x7fffffff &&
+    const bool resident_enabled = true;
+    if (resident_enabled && !trace_host && g.res_info && iters > 0 && resident_preferred(g, W, sizeof(T)) && iters <= 0x7fffffff &&
         resident_fits(g.n, W, l, ee, static_cast<int>(sizeof(T)), K)) {
         // K2: all iterations in one launch, state resident in SMEM
         ResidentArgs ra{};
@@ -1155,7 +1161,7 @@ void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count
     a.row_ptr = g.row_ptr;
     a.col = g.col;
     a.deg = deg_of<T>(g);
-    a.slots = g.slots;
+    a.order = g.order;
     a.x_in = w.X[0].p;
     a.x_out = w.X[1].p;
     a.ld = w.ld;

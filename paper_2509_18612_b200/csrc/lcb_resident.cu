@@ -142,6 +142,21 @@ __device__ __forceinline__ float2 warp_sum(float2 v) {
     v.y = warp_sum(v.y);
     return v;
 }
+__device__ __forceinline__ float sub_sum8(float v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
+}
+__device__ __forceinline__ float2 sub_sum8(float2 v) {
+    return make_float2(sub_sum8(v.x), sub_sum8(v.y));
+}
+__device__ __forceinline__ double sub_sum8(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
+}
 template <>
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -266,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
         info[j] = H + i < n ? __ldg(a.rowinfo + i) : 0u;
         vel[j] = zero_v<VT>();
     }
-    // heavy rows: COOP -> lane hs of warp w owns heavy row hs*32 + snake(w); else thread tid owns row tid
+    // heavy rows: COOP -> lane (sub*8 + hs) owns heavy row hs*128 + snake(warp*4+sub); else thread tid owns row tid
     VT vh = zero_v<VT>();
     const uint2* col4 = reinterpret_cast<const uint2*>(a.col);
     __syncthreads();
@@ -292,18 +307,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) bits[k] = 0u;
 
-        // ---- heavy rows
+        // ---- heavy rows: 8-lane subgroups, 4 rows per warp step
         if (COOP) {
-            const int hpw = (H + 31) >> 5;
-            for (int hs = 0; hs < hpw; ++hs) {
-                const int h = hs * 32 + ((hs & 1) ? 31 - warp : warp);
-                if (h >= H) continue;  // warp-uniform
-                const int2 hi = __ldg(reinterpret_cast<const int2*>(a.heavy_info) + h);
+            const int sub = lane >> 3, l8 = lane & 7;
+            const int sg = warp * 4 + sub;  // 0..127
+            const int hps = (H + 127) >> 7;
+            for (int hs = 0; hs < hps; ++hs) {
+                const int h = hs * 128 + ((hs & 1) ? 127 - sg : sg);
+                int2 hi = make_int2(0, 0);
+                if (h < H) hi = __ldg(reinterpret_cast<const int2*>(a.heavy_info) + h);
                 const int words = (hi.y + 3) >> 2;
                 VT acc = zero_v<VT>();
-                for (int q = lane; q < words; q += 32) gather4(acc, cur, __ldg(col4 + hi.x + q));
-                acc = warp_sum(acc);
-                if (lane == hs) {
+                for (int q = l8; q < words; q += 8) gather4(acc, cur, __ldg(col4 + hi.x + q));
+                acc = sub_sum8(acc);
+                if (l8 == hs && h < H) {
                     VT xo;
                     row_update_any<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err, packed);
                     nxt[h] = xo;

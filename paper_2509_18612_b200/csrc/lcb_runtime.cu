@@ -235,8 +235,12 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         std::vector<int64_t> rrp(n + 1, 0);
         for (uint32_t r = 0; r < n; ++r) rrp[r + 1] = rrp[r] + ((deg[ord[r]] + 3) & ~3);
         // heavy rows: degree > 32 (warp-cooperative in the fp32 kernel), at most 1024
+        static const int split = [] {
+            const char* e = std::getenv("LCB_HEAVY_DEG");
+            return e ? std::atoi(e) : 32;  // swept 16..192 on B200: 32 best with 8-lane groups
+        }();
         int H = 0;
-        while (H < static_cast<int>(n) && H < 1024 && deg[ord[H]] > 32) ++H;
+        while (H < static_cast<int>(n) && H < 1024 && deg[ord[H]] > split) ++H;  // 8 rows per subgroup max
         const uint32_t L = n - H;
         const uint32_t chunks = (L + 1023) / 1024 + 1;
         std::vector<int> cbase(chunks, 0);

@@ -171,6 +171,7 @@ typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference conf
     int64_t* node_updates;   /* sum over batches of n * B * l * iterations executed */
     double* step_bytes;      /* algorithmic bytes of all step launches */
     double* solve_ms;        /* CUDA-event time of the whole solve on its stream */
+    double* kernel_stats;    /* [6]: HBM-streaming K1 {ms, launches, bytes}, resident K2 {ms, launches, bytes} */
 } lcb_run_opts;
 
 /* pquco / pluco / pdeco (solver.hpp:75-86) or solve_per_component (:88-90) when

@@ -59,7 +59,7 @@ class Outcome(C.Structure):
 class RunOpts(C.Structure):
     _fields_ = [("precision", i32), ("host_init", i32), ("batched_search", i32), ("pad_", i32),
                 ("comm", P), ("step_ms", P), ("step_launches", P), ("node_updates", P),
-                ("step_bytes", P), ("solve_ms", P)]
+                ("step_bytes", P), ("solve_ms", P), ("kernel_stats", P)]
 
 
 SIGNATURES = {

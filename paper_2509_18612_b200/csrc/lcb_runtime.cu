@@ -367,6 +367,7 @@ struct Work {
     double step_bytes = 0.0;
     int64_t node_updates = 0;
     int64_t resident_iters = 0;  // iterations executed by the member-resident kernel
+    double kstats[6] = {0, 0, 0, 0, 0, 0};  // K1 {ms, launches, bytes}, K2 {ms, launches, bytes}
 
     explicit Work(int dev) : device(dev) {
         CK(cudaSetDevice(dev));
@@ -493,8 +494,12 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
         w.step_ms += ms;
         w.step_launches += 1;
-        w.step_bytes += static_cast<double>(iters) *
-                        (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+        const double bytes = static_cast<double>(iters) *
+                             (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+        w.step_bytes += bytes;
+        w.kstats[3] += ms;
+        w.kstats[4] += 1;
+        w.kstats[5] += bytes;
         w.node_updates += iters * static_cast<int64_t>(g.n) * W;
         w.resident_iters += iters;
         return r;
@@ -546,8 +551,12 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
     w.step_ms += ms;
     w.step_launches += it;
-    w.step_bytes += static_cast<double>(it) *
-                    (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+    const double bytes = static_cast<double>(it) *
+                         (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+    w.step_bytes += bytes;
+    w.kstats[0] += ms;
+    w.kstats[1] += static_cast<double>(it);
+    w.kstats[2] += bytes;
     w.node_updates += it * static_cast<int64_t>(g.n) * W;
     return r;
 }
@@ -1038,6 +1047,7 @@ void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_
         if (o.step_launches) *o.step_launches = w.step_launches;
         if (o.node_updates) *o.node_updates = w.node_updates;
         if (o.step_bytes) *o.step_bytes = w.step_bytes;
+        if (o.kernel_stats) std::memcpy(o.kernel_stats, w.kstats, sizeof(w.kstats));
     };
     if (!per_component) {
         solve_graph<T>(g, cfg, seed, o, w, sinks, assignment, out);

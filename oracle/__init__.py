@@ -104,6 +104,7 @@ def _load_orc():
         "orc_dui_init": (C.c_int, [u32, P, u64, P]),
         "orc_idi_init": (None, [u32, P, P, f64, u64, P]),
         "orc_gaussian_batch": (None, [P, i64, C.c_int, f64, i64, u64, P]),
+        "orc_gaussian_members": (None, [P, i64, C.c_int, f64, i64, i64, u64, P]),
         "orc_lifted_init_mean": (None, [u32, P, P, C.c_int, f64, C.c_int, u64, P]),
         "orc_solve": (C.c_int, [u32, P, P, P, u64, C.c_int, P, P, P, i64, P, i64, P, i64]),
         "orc_sample_population": (None, [i64, i64, f64, f64, C.c_int, u64, P, P, P]),
@@ -273,6 +274,13 @@ def gaussian_batch(mean, n: int, l: int, eta: float, B: int, key: int):
     mean = np.ascontiguousarray(mean, dtype=np.float64)
     out = np.empty(B * l * n, dtype=np.float64)
     orc.orc_gaussian_batch(_ptr(mean), n, l, eta, B, key, _ptr(out))
+    return out
+
+
+def gaussian_members(mean, n: int, l: int, eta: float, first: int, count: int, key: int):
+    mean = np.ascontiguousarray(mean, dtype=np.float64)
+    out = np.empty(count * l * n, dtype=np.float64)
+    orc.orc_gaussian_members(_ptr(mean), n, l, eta, first, count, key, _ptr(out))
     return out
 
 

@@ -315,6 +315,17 @@ void orc_gaussian_batch(const double* mean, int64_t n, int l, double eta, int64_
     }
 }
 
+void orc_gaussian_members(const double* mean, int64_t n, int l, double eta, int64_t first,
+                          int64_t count, uint64_t key, double* out) {
+    const int64_t entries = n * l;
+    const double ns = sqrt(eta);
+    for (int64_t j = 0; j < count; ++j) {
+        const uint64_t mk = split2(key, 0x6d62u, (uint64_t)(first + j));
+        double* o = out + j * entries;
+        for (int64_t k = 0; k < entries; ++k) o[k] = clamp1(mean[k] + ns * orc_normal_at(mk, (uint64_t)k));
+    }
+}
+
 void orc_lifted_init_mean(uint32_t n, const int64_t* off, const uint32_t* adj, int method,
                           double beta, int l, uint64_t key, double* mean) {
     for (int c = 0; c < l; ++c) {

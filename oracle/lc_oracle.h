@@ -71,6 +71,10 @@ void orc_idi_init(uint32_t n, const int64_t* off, const uint32_t* adj, double be
                   uint64_t key, double* x);
 void orc_gaussian_batch(const double* mean, int64_t n, int l, double eta, int64_t B,
                         uint64_t key, double* out);
+/* Members [first, first+count) of the batch above (sharding: member j's stream
+ * depends only on (key, j), init.cpp:80). */
+void orc_gaussian_members(const double* mean, int64_t n, int l, double eta, int64_t first,
+                          int64_t count, uint64_t key, double* out);
 void orc_lifted_init_mean(uint32_t n, const int64_t* off, const uint32_t* adj, int method,
                           double beta, int l, uint64_t key, double* mean);
 

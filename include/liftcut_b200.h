@@ -159,6 +159,10 @@ typedef struct lcb_outcome { /* SolveOutcome (solver.hpp:65-72) */
     double init_s, ascent_s, rounding_s, search_s, wall_s; /* StageTimes + wall */
 } lcb_outcome;
 
+/* TraceCallback (ascent.hpp:21-23) for the main batches of a solve (solver.cpp:121):
+ * called on the host after each main batch, member-major like workers=1. */
+typedef void (*lcb_trace_fn)(void* ctx, int64_t iteration, int64_t member, double objective);
+
 typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference config */
     int32_t precision;       /* lcb_precision */
     int32_t host_init;       /* -1 auto (FP64: host glibc normals, FP32: device), 0 device, 1 host */
@@ -172,6 +176,8 @@ typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference conf
     double* step_bytes;      /* algorithmic bytes of all step launches */
     double* solve_ms;        /* CUDA-event time of the whole solve on its stream */
     double* kernel_stats;    /* [6]: HBM-streaming K1 {ms, launches, bytes}, resident K2 {ms, launches, bytes} */
+    lcb_trace_fn trace_fn;   /* optional per-iteration objective trace (disables early exit) */
+    void* trace_ctx;
 } lcb_run_opts;
 
 /* pquco / pluco / pdeco (solver.hpp:75-86) or solve_per_component (:88-90) when

@@ -56,10 +56,14 @@ class Outcome(C.Structure):
                 ("rounding_s", f64), ("search_s", f64), ("wall_s", f64)]
 
 
+TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, i64, i64, f64)
+
+
 class RunOpts(C.Structure):
     _fields_ = [("precision", i32), ("host_init", i32), ("batched_search", i32), ("pad_", i32),
                 ("comm", P), ("step_ms", P), ("step_launches", P), ("node_updates", P),
-                ("step_bytes", P), ("solve_ms", P), ("kernel_stats", P)]
+                ("step_bytes", P), ("solve_ms", P), ("kernel_stats", P), ("trace_fn", TRACE_FN),
+                ("trace_ctx", P)]
 
 
 SIGNATURES = {

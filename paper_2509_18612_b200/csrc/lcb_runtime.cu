@@ -596,6 +596,8 @@ struct Solver {
     lcb_comm* comm;
     bool host_init;
     uint64_t base;
+    lcb_trace_fn trace_fn = nullptr;
+    void* trace_ctx = nullptr;
     Clock::time_point t0 = Clock::now();
     int words_n;
     int64_t B;            // local members
@@ -697,8 +699,16 @@ struct Solver {
         if (book) init_s += secs_since(mark);
 
         mark = Clock::now();
+        std::vector<double> tr;
+        const bool tracing = book && trace_fn != nullptr;
+        if (tracing) tr.assign(static_cast<size_t>(iters) * static_cast<size_t>(B), 0.0);
         const IterResult ir = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
-                                                nullptr, nullptr, static_cast<T>(mu), ee, nullptr);
+                                                nullptr, nullptr, static_cast<T>(mu), ee && !tracing,
+                                                tracing ? tr.data() : nullptr);
+        if (tracing)  // member-major, as the reference with workers=1 (ascent.cpp:52,87)
+            for (int64_t j = 0; j < B; ++j)
+                for (int64_t it = 0; it < iters; ++it)
+                    trace_fn(trace_ctx, it, member_base + j, tr[static_cast<size_t>(it * B + j)]);
         if (book) ascent_s += secs_since(mark);
         if (ir.err != ~0ull)
             fail(LCB_NUMERIC, numeric_msg(static_cast<int64_t>(ir.err & 0xffffffffull),
@@ -975,6 +985,8 @@ void solve_graph(const DevGraph& g, const lcb_config& cfg, uint64_t seed, const 
     if (g.m < 1) fail(LCB_VALIDATION, "solver requires a graph with at least one edge");
     const bool hinit = o.host_init < 0 ? (o.precision == LCB_FP64) : (o.host_init != 0);
     Solver<T> s(g, cfg, w, sinks, o.comm, hinit, seed);
+    s.trace_fn = o.trace_fn;
+    s.trace_ctx = o.trace_ctx;
     s.solve();
     s.best_assignment(z);
     out.cut_value += s.best_cut;

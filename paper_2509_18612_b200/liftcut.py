@@ -466,9 +466,9 @@ def ascend(g: Graph, state: DenseState, params: AscentParams, workers: int = 1,
                                float(params.momentum), int(bool(params.early_exit)), prec,
                                _ptr(tr), C.byref(ei), C.byref(ej))
     _check(st)
-    if trace:
-        for it in range(params.iterations):
-            for j in range(state.batch):
+    if trace:  # member-major, as the reference with workers=1
+        for j in range(state.batch):
+            for it in range(params.iterations):
                 trace(it, j, float(tr[it, j]))
 
 
@@ -776,7 +776,7 @@ class RunOptions:
 
 
 def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Algorithm,
-           opts: Optional[RunOptions], cap: int = 1 << 14) -> SolveOutcome:
+           opts: Optional[RunOptions], cap: int = 1 << 14, trace=None) -> SolveOutcome:
     opts = opts or RunOptions()
     c = cfg.to_abi()
     c.algorithm = int(algo)
@@ -795,6 +795,9 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
                       step_bytes=C.cast(C.byref(step_bytes), C.c_void_p),
                       solve_ms=C.cast(C.byref(solve_ms), C.c_void_p),
                       kernel_stats=C.cast(kst, C.c_void_p))
+    if trace is not None:
+        cb = _abi.TRACE_FN(lambda _ctx, it, member, obj: trace(int(it), int(member), float(obj)))
+        ro.trace_fn = cb
     dev = opts.comm.device if opts.comm is not None else None
     _check(_abi.lib().lcb_solve(g.handle(dev), C.byref(c), seed & _M64, int(per_component),
                                 C.byref(ro), C.byref(out), _ptr(z), bt, cap, pt, cap, st, cap))
@@ -833,7 +836,7 @@ def _pre(g: Graph, cfg: SolverConfig, need_lift: bool, name: str):
 def pquco(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1, trace=None,
           opts: Optional[RunOptions] = None) -> SolveOutcome:
     _pre(g, cfg, False, "pquco")
-    out = _solve(g, cfg, seed, False, Algorithm.pQUCO, opts)
+    out = _solve(g, cfg, seed, False, Algorithm.pQUCO, opts, trace=trace)
     out.best.algorithm = "pquco"
     return out
 
@@ -841,7 +844,7 @@ def pquco(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1, trace=None,
 def pluco(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1, trace=None,
           opts: Optional[RunOptions] = None) -> SolveOutcome:
     _pre(g, cfg, True, "pluco")
-    out = _solve(g, cfg, seed, False, Algorithm.pLUCO, opts)
+    out = _solve(g, cfg, seed, False, Algorithm.pLUCO, opts, trace=trace)
     out.best.algorithm = "pluco"
     return out
 
@@ -849,7 +852,7 @@ def pluco(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1, trace=None,
 def pdeco(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1, trace=None,
           opts: Optional[RunOptions] = None) -> SolveOutcome:
     _pre(g, cfg, True, "pdeco")
-    out = _solve(g, cfg, seed, False, Algorithm.pDECO, opts)
+    out = _solve(g, cfg, seed, False, Algorithm.pDECO, opts, trace=trace)
     out.best.algorithm = "pdeco"
     return out
 
@@ -861,7 +864,7 @@ def solve_per_component(g: Graph, cfg: SolverConfig, seed: int, workers: int = 1
         return SolveOutcome(CutSolution(np.zeros(g.node_count(), dtype=np.uint8), 0,
                                         algorithm_to_string(cfg.algorithm), seed, -1, -1),
                             [], [], [], StageTimes(), 0)
-    out = _solve(g, cfg, seed, True, cfg.algorithm, opts)
+    out = _solve(g, cfg, seed, True, cfg.algorithm, opts, trace=trace)
     out.best.algorithm = algorithm_to_string(cfg.algorithm)
     return out
 

@@ -157,12 +157,15 @@ static bool doctest_shim_match(const std::string& filter, const char* suite) {
 }
 
 int main(int argc, char** argv) {
-    std::string filter;
-    for (int i = 1; i < argc; ++i)
+    std::string filter, exclude;
+    for (int i = 1; i < argc; ++i) {
         if (std::strncmp(argv[i], "-ts=", 4) == 0) filter = argv[i] + 4;
+        if (std::strncmp(argv[i], "-tce=", 5) == 0) exclude = argv[i] + 5;  // test-case exclude
+    }
     int run = 0, failed_cases = 0;
     for (const auto& tc : ::doctest::detail::registry()) {
         if (!doctest_shim_match(filter, tc.suite)) continue;
+        if (!exclude.empty() && doctest_shim_match(exclude, tc.name)) continue;
         ++run;
         const int before = ::doctest::detail::failures();
         try {

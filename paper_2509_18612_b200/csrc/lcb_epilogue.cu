@@ -211,11 +211,12 @@ __global__ void k_argmax(const unsigned long long* __restrict__ cuts, int member
 // winner bits for key_src[0]: member (global) -> local word/bit of Z
 __global__ void k_extract_winner(const uint32_t* __restrict__ Z, int n,
                                  const unsigned long long* __restrict__ key_src,
-                                 int64_t member_base, int members, uint32_t* __restrict__ bits) {
+                                 int64_t member_base, int members, uint32_t* __restrict__ bits,
+                                 int member_offset) {
     const unsigned long long key = *key_src;
     const int64_t gm = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull));
-    const int64_t m = gm - member_base;
-    const bool local = m >= 0 && m < members;
+    const int64_t m = gm - member_base + member_offset;
+    const bool local = m >= member_offset && m < members;
     const int w = local ? static_cast<int>(m >> 5) : 0;
     const int b = local ? static_cast<int>(m & 31) : 0;
     const int words = (n + 31) / 32;
@@ -292,11 +293,12 @@ void launch_argmax(const unsigned long long* cuts, int members, int seg_size, in
 }
 
 void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* key_src,
-                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s) {
+                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s,
+                           int member_offset) {
     const int words = (n + 31) / 32;
     const int blocks = std::min((words + 7) / 8, 1024);
     count_launch();
-    k_extract_winner<<<blocks, 256, 0, s>>>(Z, n, key_src, member_base, members, bits);
+    k_extract_winner<<<blocks, 256, 0, s>>>(Z, n, key_src, member_base, members, bits, member_offset);
 }
 
 void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s) {

@@ -85,6 +85,7 @@ struct StepArgs {
     uint32_t* flags_zero;       // [members] buffer to clear for it+1
     int members;
     unsigned long long* err;    // min over (member << 32 | iteration)
+    int err_seg;                // members per error slot (0: one slot) — batched search
     T mu;
     T alpha_uniform;            // used when alpha == nullptr
     int it;
@@ -115,6 +116,7 @@ struct ResidentArgs {
     const void* alpha;       // [members] (float or double) or null
     const int* tlim;         // [members] or null
     unsigned long long* err;
+    int err_seg;             // members per error slot (0: one slot)
 };
 bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K);
 void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
@@ -148,7 +150,8 @@ void launch_argmax(const unsigned long long* cuts, int members, int seg_size,
 // winner assignment bits (node-packed, [ceil(n/32)]) of global key `key_src[seg]`;
 // zero when the winner is not local
 void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* key_src,
-                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s);
+                           int64_t member_base, int members, uint32_t* bits, cudaStream_t s,
+                           int member_offset = 0);
 void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s);
 
 // init kernels (init.cpp:20-101)

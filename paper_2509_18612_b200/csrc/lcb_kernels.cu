@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                         const T v = radd(rmul(a.mu, el(vv, e)), y);        // ascent.cpp:68
                         const T raw = radd(x, rmul(alpha, v));             // ascent.cpp:69
                         if (!isfinite(raw))                                // ascent.cpp:70-72
-                            atomicMin(a.err, (static_cast<unsigned long long>(m) << 32) |
+                            atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0), (static_cast<unsigned long long>(m) << 32) |
                                                  static_cast<unsigned>(a.it));
                         const T cl = clamp1(raw);                          // ascent.cpp:73
                         if constexpr (EE) {

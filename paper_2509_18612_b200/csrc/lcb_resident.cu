@@ -169,7 +169,7 @@ template <typename T, typename VT, int K, bool EE>
 __device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, VT& xo, int dj,
                                            const bool (&act)[K], const T (&alpha_k)[K], T mu,
                                            const int (&mem)[K], int it, uint32_t (&bits)[K],
-                                           unsigned long long* err) {
+                                           unsigned long long* const (&err)[K]) {
     const T dg = static_cast<T>(dj);
     xo = xv;
 #pragma unroll
@@ -180,7 +180,7 @@ __device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, 
         const T v = radd(rmul(mu, comp(vv, k)), y);     // v    ascent.cpp:68
         const T raw = radd(x, rmul(alpha_k[k], v));      // raw  ascent.cpp:69
         if (!isfinite(raw))                              //      ascent.cpp:70-72
-            atomicMin(err, (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
+            atomicMin(err[k], (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
         const T cl = raw < T(-1) ? T(-1) : (raw > T(1) ? T(1) : raw);  // ascent.cpp:73
         if (EE) {
             const T ch = fabs(rsub(cl, x));
@@ -196,14 +196,14 @@ __device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, 
 // Packed K=2 fp32 epilogue for the uniform path (both columns live and active).
 __device__ __forceinline__ void row_update2(const float2& xv, const float2& acc, float2& vv, float2& xo,
                                             int dj, float2 alpha2, float2 mu2, const int (&mem)[2],
-                                            int it, unsigned long long* err) {
+                                            int it, unsigned long long* const (&err)[2]) {
     const float dg = static_cast<float>(dj);
     const float2 y = fma2(make_float2(dg, dg), xv, make_float2(-acc.x, -acc.y));  // Lx
     vv = fma2(mu2, vv, y);                                                          // v
     const float2 raw = fma2(alpha2, vv, xv);                                        // raw
     if (!isfinite(raw.x) || !isfinite(raw.y)) {
         const int k = isfinite(raw.x) ? 1 : 0;
-        atomicMin(err, (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
+        atomicMin(err[k], (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
     }
     xo.x = fminf(fmaxf(raw.x, -1.f), 1.f);
     xo.y = fminf(fmaxf(raw.y, -1.f), 1.f);
@@ -213,7 +213,7 @@ template <typename T, typename VT, int K, bool EE>
 __device__ __forceinline__ void row_update_any(const VT& xv, const VT& acc, VT& vv, VT& xo, int dj,
                                                const bool (&act)[K], const T (&alpha_k)[K], T mu,
                                                const int (&mem)[K], int it, uint32_t (&bits)[K],
-                                               unsigned long long* err, bool packed) {
+                                               unsigned long long* const (&err)[K], bool packed) {
     if constexpr (K == 2 && sizeof(T) == 4 && !EE) {
         if (packed) {
             row_update2(xv, acc, vv, xo, dj, make_float2(alpha_k[0], alpha_k[1]), make_float2(mu, mu), mem, it, err);
@@ -258,6 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
         }
     }
     const T mu = static_cast<T>(sizeof(T) == 8 ? a.mu64 : a.mu);
+    unsigned long long* errp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) errp[k] = a.err + (a.err_seg ? mem[k] / a.err_seg : 0);
 
     for (int r = tid; r < n; r += kThreads) {
         const T* src = X + static_cast<int64_t>(__ldg(a.perm + r)) * a.ld + c0;
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
                 acc = sub_sum8(acc);
                 if (l8 == hs && h < H) {
                     VT xo;
-                    row_update_any<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err, packed);
+                    row_update_any<T, VT, K, EE>(cur[h], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, errp, packed);
                     nxt[h] = xo;
                 }
             }
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
             VT acc = zero_v<VT>();
             for (int q = 0; q < words; ++q) gather4(acc, cur, __ldg(col4 + hi.x + q));
             VT xo;
-            row_update<T, VT, K, EE>(cur[tid], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, a.err);
+            row_update<T, VT, K, EE>(cur[tid], acc, vh, xo, hi.y, act, alpha_k, mu, mem, it, bits, errp);
             nxt[tid] = xo;
         }
 
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
                 }
                 if (q < words) gather4(acc, cur, __ldg(cp + q));
                 VT xo;
-                row_update_any<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, a.err, packed);
+                row_update_any<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, errp, packed);
                 nxt[r] = xo;
             }
         }

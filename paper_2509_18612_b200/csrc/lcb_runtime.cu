@@ -419,7 +419,8 @@ bool resident_preferred(const DevGraph& g, int W, size_t elem) {
 }
 
 struct IterResult {
-    unsigned long long err = ~0ull;
+    unsigned long long err = ~0ull;             // slot 0 (whole batch unless segmented)
+    std::vector<unsigned long long> errs;        // one per error slot
     int final_buf = 0;
     int64_t iters = 0;
 };
@@ -429,7 +430,8 @@ struct IterResult {
 template <class T>
 IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int l, int64_t iters,
                           T alpha_u, const T* alpha_arr, const int* tlim_arr, T mu, bool ee,
-                          double* trace_host /* [iters][members] or null */) {
+                          double* trace_host /* [iters][members] or null */, int err_seg = 0) {
+    const int err_slots = err_seg > 0 ? (members + err_seg - 1) / err_seg : 1;
     StepArgs<T> a{};
     a.row_ptr = g.row_ptr;
     a.col = g.col;
@@ -445,8 +447,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     a.members = members;
     a.mu = mu;
     a.alpha_uniform = alpha_u;
-    a.err = w.err.ensure(1);
-    CK(cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), w.st));
+    a.err = w.err.ensure(static_cast<size_t>(err_slots));
+    a.err_seg = err_seg;
+    CK(cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long) * err_slots, w.st));
+    if (static_cast<size_t>(err_slots) > 1024) fail(LCB_VALIDATION, "too many error slots");
     uint32_t* F = nullptr;
     if (ee) {
         F = w.flags.ensure(static_cast<size_t>(3) * members);
@@ -481,13 +485,15 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         ra.alpha = alpha_arr;
         ra.tlim = tlim_arr;
         ra.err = a.err;
+        ra.err_seg = err_seg;
         CK(cudaEventRecord(w.ev0, w.st));
         launch_resident(ra, K, ee, static_cast<int>(sizeof(T)), w.st);
         CK(cudaEventRecord(w.ev1, w.st));
         CK(cudaGetLastError());
-        d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
+        d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
         CK(cudaStreamSynchronize(w.st));
         r.err = w.h_keys[0];
+        r.errs.assign(w.h_keys, w.h_keys + err_slots);
         r.iters = iters;
         r.final_buf = 0;
         float ms = 0.f;
@@ -542,9 +548,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     }
     CK(cudaEventRecord(w.ev1, w.st));
     CK(cudaGetLastError());
-    d2h(w.h_keys, a.err, sizeof(unsigned long long), w.st);
+    d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
     CK(cudaStreamSynchronize(w.st));
     r.err = w.h_keys[0];
+    r.errs.assign(w.h_keys, w.h_keys + err_slots);
     r.iters = it;
     r.final_buf = static_cast<int>(it & 1);
     float ms = 0.f;
@@ -598,6 +605,7 @@ struct Solver {
     uint64_t base;
     lcb_trace_fn trace_fn = nullptr;
     void* trace_ctx = nullptr;
+    bool batched_search = false;
     Clock::time_point t0 = Clock::now();
     int words_n;
     int64_t B;            // local members
@@ -630,15 +638,33 @@ struct Solver {
         CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * words_n, cudaMemcpyDeviceToDevice, w.st));
     }
 
+    // With several ranks a non-finite value on one rank must stop every rank the same
+    // way (the collectives that follow must match): min-reduce the error slots.
+    void sync_errors(IterResult& ir) {
+        if (!(comm && comm->nranks > 1)) return;
+        const size_t slots = ir.errs.size();
+        nccl_check(nccl().AllReduce(w.err.p, w.err.p, slots, ncclUint64, ncclMin, comm->comm, w.st), "allreduce(err)");
+        d2h(w.h_keys, w.err.p, sizeof(unsigned long long) * slots, w.st);
+        CK(cudaStreamSynchronize(w.st));
+        ir.errs.assign(w.h_keys, w.h_keys + slots);
+        ir.err = ir.errs[0];
+    }
+
+    // member stream keys of batch serial `s` for the local members (init.cpp:80)
+    void member_keys(int64_t s, std::vector<uint64_t>& out) const {
+        const uint64_t bkey = split2(base, 0x6261u, static_cast<uint64_t>(s));
+        for (int64_t j = 0; j < B; ++j) out.push_back(split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j)));
+    }
+
     // Host-side batch generation with glibc normals: gaussian_batch (init.cpp:69-87)
-    // for the local members, identical bits to the reference.
-    void host_batch(const std::vector<double>& mean, int l, uint64_t bkey, double noise) {
+    // for the given member streams, identical bits to the reference.
+    void host_batch(const std::vector<double>& mean, int l, const std::vector<uint64_t>& mkeys, double noise) {
         const int n = g.n;
         const size_t entries = static_cast<size_t>(n) * l;
-        std::vector<double> vals(entries * static_cast<size_t>(B));
-        for (int64_t j = 0; j < B; ++j) {
-            HostStream ms{split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j))};
-            double* o = vals.data() + static_cast<size_t>(j) * entries;
+        std::vector<double> vals(entries * mkeys.size());
+        for (size_t j = 0; j < mkeys.size(); ++j) {
+            HostStream ms{mkeys[j]};
+            double* o = vals.data() + j * entries;
             for (size_t k = 0; k < entries; ++k) {
                 const double x = mean[k] + noise * ms.normal();
                 o[k] = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
@@ -646,9 +672,24 @@ struct Solver {
         }
         double* d = w.hostbatch.ensure(vals.size());
         h2d(d, vals.data(), sizeof(double) * vals.size(), w.st);
-        launch_transpose_in<T>(d, w.X[0].p, n, static_cast<int>(B * l), w.ld, w.st);
+        launch_transpose_in<T>(d, w.X[0].p, n, static_cast<int>(mkeys.size() * l), w.ld, w.st);
         CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(n) * w.ld, w.st));
         CK(cudaStreamSynchronize(w.st));  // vals is pageable and goes out of scope
+    }
+
+    // batch init around a device mean or pm1(bits): glibc normals on the host or the
+    // device Box-Muller kernel
+    void init_batch(int l, const double* dmean, const uint32_t* bits, const std::vector<uint64_t>& mk,
+                    double noise) {
+        if (host_init) {
+            host_batch(host_mean_from(dmean, bits, l), l, mk, noise);
+        } else {
+            uint64_t* dk = w.mkeys.ensure(mk.size());
+            h2d(dk, mk.data(), sizeof(uint64_t) * mk.size(), w.st);
+            launch_gaussian<T>(w.X[0].p, w.V.p, w.ld, g.n, static_cast<int>(mk.size()), l, dk, dmean, bits,
+                               cfg.init_scale, noise, w.st);
+            CK(cudaStreamSynchronize(w.st));  // mk is pageable
+        }
     }
 
     std::vector<double> host_mean_from(const double* dmean, const uint32_t* bits, int l) {
@@ -678,33 +719,25 @@ struct Solver {
                        int64_t iters, double mu, bool ee, bool book) {
         const int n = g.n;
         const int64_t s = serial++;
-        const uint64_t bkey = split2(base, 0x6261u, static_cast<uint64_t>(s));
         const double eta_eff = cfg.scale_noise ? cfg.eta / (cfg.init_scale * cfg.init_scale) : cfg.eta;
         const double noise = std::sqrt(eta_eff);
         const int W = static_cast<int>(B * l);
         w.shape(n, W);
 
         auto mark = Clock::now();
-        if (host_init) {
-            host_batch(host_mean_from(dmean, bits, l), l, bkey, noise);
-        } else {
-            std::vector<uint64_t> mk(static_cast<size_t>(B));
-            for (int64_t j = 0; j < B; ++j) mk[j] = split2(bkey, 0x6d62u, static_cast<uint64_t>(member_base + j));
-            uint64_t* dk = w.mkeys.ensure(mk.size());
-            h2d(dk, mk.data(), sizeof(uint64_t) * mk.size(), w.st);
-            launch_gaussian<T>(w.X[0].p, w.V.p, w.ld, n, static_cast<int>(B), l, dk, dmean, bits,
-                               cfg.init_scale, noise, w.st);
-            CK(cudaStreamSynchronize(w.st));  // mk is pageable
-        }
+        std::vector<uint64_t> mk;
+        member_keys(s, mk);
+        init_batch(l, dmean, bits, mk, noise);
         if (book) init_s += secs_since(mark);
 
         mark = Clock::now();
         std::vector<double> tr;
         const bool tracing = book && trace_fn != nullptr;
         if (tracing) tr.assign(static_cast<size_t>(iters) * static_cast<size_t>(B), 0.0);
-        const IterResult ir = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
-                                                nullptr, nullptr, static_cast<T>(mu), ee && !tracing,
-                                                tracing ? tr.data() : nullptr);
+        IterResult ir = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
+                                          nullptr, nullptr, static_cast<T>(mu), ee && !tracing,
+                                          tracing ? tr.data() : nullptr);
+        sync_errors(ir);
         if (tracing)  // member-major, as the reference with workers=1 (ascent.cpp:52,87)
             for (int64_t j = 0; j < B; ++j)
                 for (int64_t it = 0; it < iters; ++it)
@@ -739,6 +772,86 @@ struct Solver {
         r.serial = s;
         if (book) rounding_s += secs_since(mark);
         return r;
+    }
+
+    // Batched evolve() round: K candidates' batches in one launch
+    // sequence.  Candidate k keeps serial serial0+k (its member streams are the ones
+    // the sequential order would have drawn), its own (alpha, T) per member, its own
+    // error slot and argmax segment; the segments' keys come back in one copy.
+    struct MultiRes {
+        std::vector<BatchRes> res;
+        std::vector<bool> numeric;
+        unsigned long long* d_keys = nullptr;
+        uint32_t* Z = nullptr;
+    };
+    MultiRes run_batch_multi(bool lifted, int l, const uint32_t* bits, const std::vector<Cand*>& cs, double mu,
+                             bool ee) {
+        const int n = g.n;
+        const int K = static_cast<int>(cs.size());
+        const int64_t serial0 = serial;
+        serial += K;
+        const double eta_eff = cfg.scale_noise ? cfg.eta / (cfg.init_scale * cfg.init_scale) : cfg.eta;
+        const int members = static_cast<int>(B) * K;
+        const int W = members * l;
+        w.shape(n, W);
+        std::vector<uint64_t> mk;
+        for (int k = 0; k < K; ++k) member_keys(serial0 + k, mk);
+        init_batch(l, nullptr, bits, mk, std::sqrt(eta_eff));
+        std::vector<T> alpha(static_cast<size_t>(members));
+        std::vector<int> tlim(static_cast<size_t>(members));
+        int64_t tmax = 0, upd = 0;
+        for (int k = 0; k < K; ++k) {
+            tmax = std::max(tmax, cs[k]->iterations);
+            upd += cs[k]->iterations;
+            for (int64_t j = 0; j < B; ++j) {
+                alpha[static_cast<size_t>(k * B + j)] = static_cast<T>(cs[k]->alpha());
+                tlim[static_cast<size_t>(k * B + j)] = static_cast<int>(cs[k]->iterations);
+            }
+        }
+        T* da = w.alpha.ensure(alpha.size());
+        int* dt = w.tlim.ensure(tlim.size());
+        h2d(da, alpha.data(), sizeof(T) * alpha.size(), w.st);
+        h2d(dt, tlim.data(), sizeof(int) * tlim.size(), w.st);
+        const int64_t before = w.node_updates;
+        IterResult ir = run_iterations<T>(g, w, W, members, l, tmax, T(0), da, dt, static_cast<T>(mu), ee,
+                                          nullptr, static_cast<int>(B));
+        sync_errors(ir);
+        w.node_updates = before + upd * static_cast<int64_t>(n) * B * l;  // active updates only
+        MultiRes out;
+        const int words = (members + 31) / 32;
+        out.Z = w.Z.ensure(static_cast<size_t>(words) * n);
+        launch_round_pack<T>(w.X[ir.final_buf].p, w.ld, n, members, l, lifted ? 1 : 0, out.Z, w.st);
+        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32);
+        launch_cut_count(g, out.Z, words, cuts, w.st);
+        out.d_keys = w.keys.ensure(static_cast<size_t>(std::max(K, 8)));
+        launch_argmax(cuts, members, static_cast<int>(B), member_base, out.d_keys, w.st);
+        if (comm && comm->nranks > 1)
+            nccl_check(nccl().AllReduce(out.d_keys, out.d_keys, static_cast<size_t>(K), ncclUint64, ncclMax,
+                                        comm->comm, w.st),
+                       "allreduce(keys)");
+        d2h(w.h_keys, out.d_keys, sizeof(unsigned long long) * K, w.st);
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+        for (int k = 0; k < K; ++k) {
+            const unsigned long long key = w.h_keys[k];
+            BatchRes r;
+            r.cut = static_cast<int64_t>(key >> 32);
+            r.member = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull));
+            r.serial = serial0 + k;
+            out.res.push_back(r);
+            out.numeric.push_back(k < static_cast<int>(ir.errs.size()) && ir.errs[k] != ~0ull);
+        }
+        return out;
+    }
+
+    // winner bits of segment k of the last multi batch -> w.win
+    void multi_winner(const MultiRes& m, int k) {
+        launch_extract_winner(m.Z, g.n, m.d_keys + k, member_base, static_cast<int>(B) * (k + 1), w.win.p, w.st,
+                              static_cast<int>(B) * k);
+        if (comm && comm->nranks > 1)
+            nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
+                                        comm->comm, w.st),
+                       "allreduce(winner)");
     }
 
     // note_batch — solver.cpp:145-150 (winner bits are in w.win)
@@ -783,9 +896,49 @@ struct Solver {
             c.exponent = s.uniform(cfg.e_lower, cfg.e_upper);
         }
         const size_t half = pop.size() / 2;
+        auto trace_eval = [&](int round, const Cand& c) {
+            if (sinks.nst < sinks.st_cap) {
+                lcb_search_trace& e = sinks.st[sinks.nst];
+                e.round = round;
+                e.pad_ = 0;
+                e.exponent = c.exponent;
+                e.iterations = c.iterations;
+                e.fitness = c.fitness;
+            }
+            ++sinks.nst;
+        };
         for (int round = 1; round <= cfg.rounds; ++round) {
-            for (Cand& c : pop) {
-                if (c.has_fit) continue;
+            std::vector<Cand*> todo;
+            for (Cand& c : pop)
+                if (!c.has_fit) todo.push_back(&c);
+            if (batched_search && todo.size() > 1) {
+                // one budget check per round (the sequential order checks per candidate)
+                if (budget_gone()) {
+                    for (Cand* c : todo) {
+                        c->has_fit = true;
+                        c->fitness = -std::numeric_limits<double>::infinity();
+                        trace_eval(round, *c);
+                    }
+                } else {
+                    const MultiRes m = run_batch_multi(lifted, l, w.recenter.p, todo, mu, ee);
+                    for (size_t k = 0; k < todo.size(); ++k) {
+                        Cand& c = *todo[k];
+                        double fit = -std::numeric_limits<double>::infinity();
+                        if (!m.numeric[k]) {
+                            const BatchRes& r = m.res[k];
+                            if (!has_best || r.cut > best_cut) multi_winner(m, static_cast<int>(k));
+                            note_batch(r, 1, c.alpha(), c.iterations);
+                            fit = static_cast<double>(r.cut);
+                        }
+                        c.has_fit = true;
+                        c.fitness = fit;
+                        trace_eval(round, c);
+                    }
+                }
+                todo.clear();
+            }
+            for (Cand* cp : todo) {
+                Cand& c = *cp;
                 double fit;
                 if (budget_gone()) {
                     fit = -std::numeric_limits<double>::infinity();  // Error -> -inf
@@ -801,15 +954,7 @@ struct Solver {
                 }
                 c.has_fit = true;
                 c.fitness = fit;
-                if (sinks.nst < sinks.st_cap) {
-                    lcb_search_trace& e = sinks.st[sinks.nst];
-                    e.round = round;
-                    e.pad_ = 0;
-                    e.exponent = c.exponent;
-                    e.iterations = c.iterations;
-                    e.fitness = fit;
-                }
-                ++sinks.nst;
+                trace_eval(round, c);
             }
             std::stable_sort(pop.begin(), pop.end(), ranks_before);
             for (size_t slot = half; slot < pop.size(); ++slot) {
@@ -987,6 +1132,7 @@ void solve_graph(const DevGraph& g, const lcb_config& cfg, uint64_t seed, const 
     Solver<T> s(g, cfg, w, sinks, o.comm, hinit, seed);
     s.trace_fn = o.trace_fn;
     s.trace_ctx = o.trace_ctx;
+    s.batched_search = o.batched_search != 0;
     s.solve();
     s.best_assignment(z);
     out.cut_value += s.best_cut;

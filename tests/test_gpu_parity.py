@@ -340,3 +340,35 @@ def test_resident_isolated_and_heavy_rows_fp64_bitwise():
         for j in range(40):
             a_, b_ = got32[j * n:(j + 1) * n], w5[j * n:(j + 1) * n]
             assert np.max(np.abs(a_ - b_)) / np.max(np.abs(b_)) <= FP32_NORM_TOL
+
+
+def test_batched_search_rounds_match_sequential_and_reference(golden):
+    """evolve() rounds evaluated as one multi-candidate launch keep every serial,
+    stream, fitness and trace of the sequential order (no time budget)."""
+    d = golden("solver_records.json")
+    n_search = 0
+    for c in d["cases"]:
+        if not c["config"]["has_search"]:
+            continue
+        n_search += 1
+        off, adj = d["graphs"][c["graph"]]
+        g = lc.Graph.from_csr(len(off) - 1, off, adj)
+        cfg = product_config(c["config"])
+        fn = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[cfg.algorithm]
+        r = fn(g, cfg, c["seed"], opts=lc.RunOptions(precision=LCB_FP64, batched_search=True))
+        assert r.best.cut_value == c["cut"] and r.best.assignment.tolist() == c["assignment"]
+        assert [[e.serial, 0 if e.kind == "main" else 1, e.alpha, e.iterations, e.batch_best, e.best_so_far]
+                for e in r.batch_trace] == c["batch_trace"]
+        assert [[e.round, e.exponent, e.iterations, e.fitness] for e in r.search_trace] == c["search_trace"]
+    assert n_search >= 2
+    # a larger population through both paths
+    cg = O.generate_er(300, 0.03, 3)
+    cfg = lc.SolverConfig(batch_size=64, num_batches=2, ascent=lc.AscentParams(0.05, 60),
+                          search=lc.SearchConfig(20, 80, -3.0, -1.0, 6, 3))
+    a = lc.pquco(pg(cg), cfg, 11, opts=lc.RunOptions(precision=LCB_FP64, batched_search=False))
+    b = lc.pquco(pg(cg), cfg, 11, opts=lc.RunOptions(precision=LCB_FP64, batched_search=True))
+    assert a.best.cut_value == b.best.cut_value and a.batch_trace == b.batch_trace
+    assert a.search_trace == b.search_trace and np.array_equal(a.best.assignment, b.best.assignment)
+    w = O.solve(cg, O.default_config(batch_size=64, num_batches=2, iterations=60, has_search=1, t_lower=20,
+                                     t_upper=80, e_lower=-3.0, e_upper=-1.0, population_size=6, rounds=3), 11)
+    assert b.best.cut_value == w.cut_value and b.best.assignment.tolist() == w.assignment.tolist()

@@ -196,6 +196,9 @@ int lcb_comm_unique_id(uint8_t id[128]);
 int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device,
                     lcb_comm** out);
 void lcb_comm_destroy(lcb_comm* c);
+/* Solves keep their device workspaces in a per-(device, precision) pool for reuse;
+ * this frees every pooled workspace (e.g. before a large allocation elsewhere). */
+void lcb_release_workspaces(void);
 /* process-wide counters: kernel launches and host<->device bytes since load */
 void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* host helpers shared with the CPU tests of the exchange */

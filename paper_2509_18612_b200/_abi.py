@@ -86,6 +86,7 @@ SIGNATURES = {
     "lcb_comm_create": (C.c_int, [P, i32, i32, C.c_int, C.POINTER(P)]),
     "lcb_comm_destroy": (None, [P]),
     "lcb_counters": (None, [P, P, P]),
+    "lcb_release_workspaces": (None, []),
     "lcb_pack_key": (u64, [i64, i64]),
     "lcb_unpack_key": (None, [u64, P, P]),
 }

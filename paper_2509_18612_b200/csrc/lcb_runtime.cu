@@ -20,6 +20,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <optional>
 #include <string>
@@ -400,6 +401,51 @@ struct Work {
         }
         return h_flags;
     }
+};
+
+// Workspaces are pooled per (device, precision): a solve takes one, returns it on exit,
+// so repeated solves (bench steps, per-component solves, service use) reuse the
+// stream, events, pinned staging and device buffers instead of re-allocating them.
+template <class T>
+struct WorkPool {
+    std::mutex mu;
+    std::vector<std::unique_ptr<Work<T>>> free_list;
+    static WorkPool& get() {
+        static WorkPool p;
+        return p;
+    }
+};
+
+template <class T>
+struct PooledWork {
+    std::unique_ptr<Work<T>> w;
+    explicit PooledWork(int device) {
+        auto& p = WorkPool<T>::get();
+        {
+            std::lock_guard<std::mutex> lk(p.mu);
+            for (size_t i = 0; i < p.free_list.size(); ++i)
+                if (p.free_list[i]->device == device) {
+                    w = std::move(p.free_list[i]);
+                    p.free_list.erase(p.free_list.begin() + static_cast<std::ptrdiff_t>(i));
+                    break;
+                }
+        }
+        if (!w) w = std::make_unique<Work<T>>(device);
+        w->step_ms = 0.0;
+        w->step_launches = 0;
+        w->step_bytes = 0.0;
+        w->node_updates = 0;
+        w->resident_iters = 0;
+        for (double& k : w->kstats) k = 0.0;
+    }
+    ~PooledWork() {
+        if (!w) return;
+        cudaStreamSynchronize(w->st);
+        auto& p = WorkPool<T>::get();
+        std::lock_guard<std::mutex> lk(p.mu);
+        p.free_list.push_back(std::move(w));
+    }
+    Work<T>& operator*() { return *w; }
 };
 
 // Kernel choice measured on B200 (profiles/round1_kernel_ab.md): the member-resident
@@ -1177,7 +1223,8 @@ std::vector<std::vector<uint32_t>> components(const DevGraph& g) {
 template <class T>
 void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_component,
                const lcb_run_opts& o, lcb_outcome& out, uint8_t* assignment, TraceSinks& sinks) {
-    Work<T> w(g.device);
+    PooledWork<T> pw(g.device);
+    Work<T>& w = *pw;
     const auto t0 = Clock::now();
     std::memset(&out, 0, sizeof(out));
     cudaEvent_t s0 = nullptr, s1 = nullptr;
@@ -1297,7 +1344,8 @@ void ascend_host(const DevGraph& g, double* values, int64_t n, int l, int64_t B,
     if (W64 > (1 << 26)) fail(LCB_VALIDATION, "batch too wide");
     const int W = static_cast<int>(W64);
     DeviceScope ds(g.device);
-    Work<T> w(g.device);
+    PooledWork<T> pw(g.device);
+    Work<T>& w = *pw;
     w.shape(g.n, W);
     const size_t count = static_cast<size_t>(W) * g.n;
     double* d = w.hostbatch.ensure(count);
@@ -1323,7 +1371,8 @@ template <class T>
 void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count) {
     const int W = static_cast<int>(count);
     DeviceScope ds(g.device);
-    Work<T> w(g.device);
+    PooledWork<T> pw(g.device);
+    Work<T>& w = *pw;
     w.shape(g.n, W);
     const size_t cells = static_cast<size_t>(W) * g.n;
     double* d = w.hostbatch.ensure(cells);
@@ -1434,7 +1483,8 @@ int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t*
             if (z[i] > 1) fail(LCB_VALIDATION, "cut_value: assignment entries must be 0 or 1");
         if (count < 1) return;
         DeviceScope ds(G.device);
-        Work<double> w(G.device);
+        PooledWork<double> pw(G.device);
+        Work<double>& w = *pw;
         uint8_t* dz = reinterpret_cast<uint8_t*>(w.hostbatch.ensure((cells + 7) / 8));
         h2d(dz, z, cells, w.st);
         const int words = static_cast<int>((count + 31) / 32);
@@ -1457,7 +1507,8 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
         const DevGraph& G = g->g;
         if (l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
         DeviceScope ds(G.device);
-        Work<double> w(G.device);
+        PooledWork<double> pw(G.device);
+        Work<double>& w = *pw;
         const int W = static_cast<int>(B * l);
         w.shape(G.n, W);
         const size_t cells = static_cast<size_t>(W) * G.n;
@@ -1493,7 +1544,8 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
 static void init_mean_host(const DevGraph& G, int method, double beta, int l, const uint64_t* ck,
                            double scale, double* out) {
     DeviceScope ds(G.device);
-    Work<double> w(G.device);
+    PooledWork<double> pw(G.device);
+        Work<double>& w = *pw;
     uint64_t* dck = w.colkeys.ensure(static_cast<size_t>(l));
     h2d(dck, ck, sizeof(uint64_t) * l, w.st);
     double* mean = w.mean.ensure(static_cast<size_t>(G.n) * l);
@@ -1533,7 +1585,8 @@ int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, dou
         if (eta <= 0.0) fail(LCB_VALIDATION, "gaussian_batch: eta must be > 0");
         if (n < 1 || l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
         DeviceScope ds(device);
-        Work<double> w(device);
+        PooledWork<double> pw(device);
+        Work<double>& w = *pw;
         const int W = static_cast<int>(B * l);
         w.shape(static_cast<int>(n), W);
         double* dm = w.mean.ensure(static_cast<size_t>(n) * l);
@@ -1603,6 +1656,15 @@ void lcb_comm_destroy(lcb_comm* c) {
     if (!c) return;
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     delete c;
+}
+
+void lcb_release_workspaces(void) {
+    for (auto* fl : {&WorkPool<float>::get().free_list}) {
+        std::lock_guard<std::mutex> lk(WorkPool<float>::get().mu);
+        fl->clear();
+    }
+    std::lock_guard<std::mutex> lk(WorkPool<double>::get().mu);
+    WorkPool<double>::get().free_list.clear();
 }
 
 void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes) {

@@ -255,7 +255,7 @@ def run_b200(args):
         comm = Comm.from_torch(local)
     prec = LCB_FP32 if args.precision == "fp32" else LCB_FP64
     g, cfg, desc = workload(args.config, world, args.precision)
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=comm)
+    opts = lc.RunOptions(precision=prec, host_init=0, comm=comm, batched_search=True)
     solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[int(cfg.algorithm)]
     g.handle(local)  # inputs resident in HBM before timing
 

@@ -687,7 +687,7 @@ struct Solver {
     // With several ranks a non-finite value on one rank must stop every rank the same
     // way (the collectives that follow must match): min-reduce the error slots.
     void sync_errors(IterResult& ir) {
-        if (!(comm && comm->nranks > 1)) return;
+        if (!(comm && comm->comm)) return;
         const size_t slots = ir.errs.size();
         nccl_check(nccl().AllReduce(w.err.p, w.err.p, slots, ncclUint64, ncclMin, comm->comm, w.st), "allreduce(err)");
         d2h(w.h_keys, w.err.p, sizeof(unsigned long long) * slots, w.st);
@@ -801,10 +801,10 @@ struct Solver {
         launch_cut_count(g, Z, words, cuts, w.st);
         unsigned long long* key = w.keys.ensure(8);
         launch_argmax(cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
-        if (comm && comm->nranks > 1)
+        if (comm && comm->comm)
             nccl_check(nccl().AllReduce(key, key, 1, ncclUint64, ncclMax, comm->comm, w.st), "allreduce(key)");
         launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
-        if (comm && comm->nranks > 1)
+        if (comm && comm->comm)
             nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
                                         comm->comm, w.st),
                        "allreduce(winner)");
@@ -871,7 +871,7 @@ struct Solver {
         launch_cut_count(g, out.Z, words, cuts, w.st);
         out.d_keys = w.keys.ensure(static_cast<size_t>(std::max(K, 8)));
         launch_argmax(cuts, members, static_cast<int>(B), member_base, out.d_keys, w.st);
-        if (comm && comm->nranks > 1)
+        if (comm && comm->comm)
             nccl_check(nccl().AllReduce(out.d_keys, out.d_keys, static_cast<size_t>(K), ncclUint64, ncclMax,
                                         comm->comm, w.st),
                        "allreduce(keys)");
@@ -894,7 +894,7 @@ struct Solver {
     void multi_winner(const MultiRes& m, int k) {
         launch_extract_winner(m.Z, g.n, m.d_keys + k, member_base, static_cast<int>(B) * (k + 1), w.win.p, w.st,
                               static_cast<int>(B) * k);
-        if (comm && comm->nranks > 1)
+        if (comm && comm->comm)
             nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
                                         comm->comm, w.st),
                        "allreduce(winner)");
@@ -1641,7 +1641,8 @@ int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int dev
         c->nranks = nranks;
         c->rank = rank;
         c->device = device;
-        if (nranks > 1) {
+        const char* force = std::getenv("LCB_FORCE_NCCL");  // 1-rank communicator: exercise the NCCL path
+        if (nranks > 1 || (force && force[0] == '1')) {
             if (!nccl().ok) fail(LCB_CUDA, "NCCL unavailable: " + nccl().why);
             DeviceScope ds(device);
             ncclUniqueId u;

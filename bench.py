@@ -76,6 +76,11 @@ def workload(name, nranks, precision):
         cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=64,
                               ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1)
         desc = "ER n=800 p=0.015 seed0 (ref generator), pQUCO B=64, T=500, 1 batch"
+    elif name == "c3":
+        g = lc.generate_er(20_000, 0.5, 0)
+        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=256,
+                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1)
+        desc = "dense ER n=20k p=0.5 (ref generator, ~1e8 edges), pQUCO B=256, T=500, tensor-core path"
     elif name == "c4":
         g = er_sparse(1_000_000, 10.0, 0)
         cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=512 // nranks if nranks > 1 else 512,
@@ -154,6 +159,17 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def measured_tensor_peak():
+    """Dense bf16 peak from MEASURED_PEAKS.json: the sustained figure (the dense
+    kernel runs back to back for the whole step)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops_sustained", d.get("bf16_tflops", 1590.0)), "measured (sustained)"
+    return 1590.0, "fallback"
+
+
 def ncu_traffic(config, precision, kernel):
     """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed
     ncu capture of this workload (profiles/ncu_summary.json), if any."""
@@ -197,7 +213,7 @@ def cpu_reference_step(g, cfg, nranks, t_sample):
 def ref_sample_T(name):
     # ~10-20 s of host work per sample on 8 cores; long enough that per-batch
     # init/rounding stays a minor share, as it is at the full T
-    return {"c1": 500, "c4": 2, "c5": 5}.get(name, 20)
+    return {"c1": 500, "c3": 1, "c4": 2, "c5": 5}.get(name, 20)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -273,7 +289,7 @@ def run_b200(args):
     sampler = ClockSampler(local) if rank == 0 else None
     l0 = lc.counters()[0]
     dev_ms, step_ms, step_bytes, launches, ups, best = 0.0, 0.0, 0.0, 0, 0, 0
-    kst = {"k_step": [0.0, 0.0, 0.0], "k_resident": [0.0, 0.0, 0.0]}
+    kst = {"k_step": [0.0, 0.0, 0.0], "k_resident": [0.0, 0.0, 0.0], "k_dense_step": [0.0, 0.0, 0.0]}
     for k in range(args.steps):
         flush.fill_(k & 0xFF)  # L2 flush between timed steps (untimed)
         barrier()
@@ -317,10 +333,24 @@ def run_b200(args):
         peak, which = measured_peaks()
         # roofline of the dominant step kernel (largest share of step-kernel time)
         kname = max(kst, key=lambda k: kst[k][0])
-        k_ms, k_launch, k_bytes = kst[kname]
-        achieved = k_bytes / (k_ms / 1e3) / 1e9
-        per_launch = k_bytes / max(k_launch, 1)
+        k_ms, k_launch, k_amount = kst[kname]
         shares = {k: v[0] / max(step_ms, 1e-9) for k, v in kst.items() if v[1]}
+        if kname == "k_dense_step":
+            tpeak, twhich = measured_tensor_peak()
+            achieved = k_amount / (k_ms / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": achieved / tpeak, "traffic": ncu_traffic(args.config, args.precision, kname),
+                    "kernel": kname, "algorithmic_flops_per_launch": k_amount / max(k_launch, 1),
+                    "executed_tflops": 3 * achieved, "executed_frac": 3 * achieved / tpeak,
+                    "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": twhich,
+                    "model": "2*n^2*W flops per iteration (SURVEY 8d); executed = 3x (bf16 hi/mid/lo planes)"}
+        else:
+            achieved = k_amount / (k_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": ncu_traffic(args.config, args.precision, kname),
+                    "kernel": kname, "algorithmic_bytes_per_launch": k_amount / max(k_launch, 1),
+                    "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": which,
+                    "model": "16 B/node-update fp32 (32 fp64) + CSR bytes per iteration (SURVEY 8d)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             T = ref_sample_T(args.config)
@@ -344,12 +374,7 @@ def run_b200(args):
                        "l2": "flushed between timed steps (512 MB write); each step is a full solve",
                        "parallelism": f"member-sharded dp{world}" if world > 1 else "single GPU",
                        "timing": "CUDA events on the solver stream, sum over steps, max over ranks"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.config, args.precision, kname),
-                         "kernel": kname, "algorithmic_bytes_per_launch": per_launch,
-                         "ms_per_launch": k_ms / max(k_launch, 1),
-                         "step_time_share": shares, "peak_source": which,
-                         "model": "16 B/node-update fp32 (32 fp64) + CSR bytes per iteration (SURVEY 8d)"},
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": (h1 - h0) // args.steps,
                     "d2h_bytes_per_step": (d1 - d0) // args.steps},
@@ -371,7 +396,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

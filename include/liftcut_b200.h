@@ -175,7 +175,8 @@ typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference conf
     int64_t* node_updates;   /* sum over batches of n * B * l * iterations executed */
     double* step_bytes;      /* algorithmic bytes of all step launches */
     double* solve_ms;        /* CUDA-event time of the whole solve on its stream */
-    double* kernel_stats;    /* [6]: HBM-streaming K1 {ms, launches, bytes}, resident K2 {ms, launches, bytes} */
+    double* kernel_stats;    /* [9]: K1 HBM-streaming {ms, launches, bytes}, K2 resident {ms, launches, bytes},
+                                K3 dense tensor-core {ms, launches, algorithmic flops} */
     lcb_trace_fn trace_fn;   /* optional per-iteration objective trace (disables early exit) */
     void* trace_ctx;
 } lcb_run_opts;

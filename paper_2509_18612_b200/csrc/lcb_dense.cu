@@ -1,0 +1,436 @@
+// lcb_dense.cu — K3: dense-graph PGA step on the 5th-generation tensor cores.
+//
+// For dense graphs (config 3: ER n=20k p=0.5) the Laplacian product is a GEMM
+//   D[v][c] = sum_u A[v][u] X[u][c]      (M = n nodes, N = W columns, K = n)
+// with A the 0/1 adjacency — exact in bf16.  X (fp32) is split exactly into three
+// bf16 planes hi + mid + lo (8 significand bits each = all 24 of fp32); the three
+// products accumulate into ONE fp32 accumulator in tensor memory, so the sum is an
+// fp32-faithful A·X (executed flops = 3x algorithmic).
+//
+// One CTA per 128-row tile of A (M=128), all N = W (<= 256) columns:
+//   warp 0  TMA producer: A tile [128 x 64] + 3 plane tiles [W x 64] per K step,
+//           128-byte swizzle, 2-stage ring, mbarrier complete_tx;
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16 x bf16
+//           -> fp32, 12 MMAs of K=16 per K step), tcgen05.commit frees ring slots and
+//           finally signals the epilogue;
+//   warps 2-5 epilogue: tcgen05.ld 32 columns at a time, fused
+//           y = deg*x - Ax; v = mu v + y; raw = x + alpha v; finite check; clamp
+//           (ascent.cpp:66-77), writes x' / v' (fp32, member-major [W][n]) and the
+//           three bf16 planes of x' for the next iteration (planes double-buffered:
+//           every CTA reads all of them).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "lcb_internal.h"
+
+namespace lcb {
+
+namespace {
+
+constexpr int kBM = 128;                          // rows of A per CTA (UMMA M)
+constexpr int kBK = 64;                           // K per stage (64 bf16 = one 128-byte swizzle row)
+constexpr int kStages = 2;
+constexpr int kATileBytes = kBM * kBK * 2;        // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);       // start address
+    d |= static_cast<uint64_t>(1u) << 16;                      // LBO (unused for swizzled K-major) = 16 B
+    d |= static_cast<uint64_t>(1024u >> 4) << 32;              // SBO = 1024 B between 8-row groups
+    d |= static_cast<uint64_t>(1u) << 46;                      // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2u) << 61;                      // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4)                                   // D format F32
+           | (1u << 7)                                 // A BF16
+           | (1u << 10)                                // B BF16
+           | (static_cast<uint32_t>(N >> 3) << 17)     // N >> 3
+           | (static_cast<uint32_t>(M >> 4) << 24);    // M >> 4
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// exact split of an fp32 value into three bf16 (truncating each remainder is exact:
+// x - bf16(x) is representable in fp32 and has <= 16 significant bits left)
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
+    h = __float2bfloat16_rz(x);
+    const float r1 = x - __bfloat162float(h);
+    m = __float2bfloat16_rz(r1);
+    const float r2 = r1 - __bfloat162float(m);
+    l = __float2bfloat16_rn(r2);
+}
+
+struct DenseArgs {
+    const float* deg;        // [n]
+    float* X;                // [W][n] member-major fp32 iterate (in place)
+    float* V;                // [W][n] velocity (in place)
+    __nv_bfloat16* planes_out;  // [3][W][ldp] planes of x' for the next iteration
+    int n;
+    int ldx;                 // row pitch of X / V (elements)
+    int ldp;                 // row pitch of the planes (elements, multiple of 8)
+    int W;                   // live columns (<= 256, multiple of 16)
+    int l;
+    int col_base;            // first batch column of this launch (column chunks of <= 256)
+    float mu;
+    float alpha_uniform;
+    const float* alpha;      // [members] or null
+    const int* tlim;         // [members] or null
+    unsigned long long* err;
+    int err_seg;
+    int it;
+};
+
+template <int N>
+__global__ void __launch_bounds__(192, 1)
+    k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP, DenseArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile
+    constexpr int kStageBytes = kATileBytes + 3 * kPlaneTile;
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], acc_bar;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * kBM;
+    const int nk = (a.n + kBK - 1) / kBK;
+    // 1024-byte aligned ring
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(&acc_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            for (int k = 0; k < nk; ++k) {
+                const int s = k % kStages;
+                if (k >= kStages) mbar_wait(&empty_bar[s], ((k / kStages) - 1) & 1);
+                uint8_t* st = ring + s * kStageBytes;
+                mbar_expect_tx(&full_bar[s], kStageBytes);
+                tma_load_2d(st, &tmA, &full_bar[s], k * kBK, m0);
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+                    tma_load_2d(st + kATileBytes + p * kPlaneTile, &tmP, &full_bar[s], k * kBK, p * a.W);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        constexpr uint32_t idesc = idesc_bf16(kBM, N);
+        if (lane == 0) {
+            for (int k = 0; k < nk; ++k) {
+                const int s = k % kStages;
+                mbar_wait(&full_bar[s], (k / kStages) & 1);
+                tc_fence_after();
+                const uint32_t st = smem_u32(ring + s * kStageBytes);
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t da = umma_desc_k_sw128(st + kk * 32);
+                        const uint64_t db = umma_desc_k_sw128(st + kATileBytes + p * kPlaneTile + kk * 32);
+                        umma_bf16(tmem, da, db, idesc, (k | p | kk) != 0);
+                    }
+                umma_commit(&empty_bar[s]);  // slot free once these MMAs have read it
+            }
+            umma_commit(&acc_bar);           // accumulator complete
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 2..5): TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        const int row = m0 + q * 32 + lane;
+        mbar_wait(&acc_bar, 0);
+        tc_fence_after();
+        const bool live = row < a.n;
+        const float dg = live ? __ldg(a.deg + row) : 0.f;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
+            if (!live) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int c = c0 + j;
+                if (c >= a.W) continue;
+                const int m = (a.col_base + c) / a.l;
+                bool act = true;
+                float alpha = a.alpha_uniform;
+                if (a.tlim) act = a.it < __ldg(a.tlim + m);
+                if (a.alpha) alpha = __ldg(a.alpha + m);
+                float* xp = a.X + static_cast<int64_t>(c) * a.ldx + row;
+                float* vp = a.V + static_cast<int64_t>(c) * a.ldx + row;
+                float x = *xp;
+                if (act) {
+                    const float ax = __uint_as_float(r[j]);
+                    const float y = dg * x - ax;          // Lx    (graph.cpp:120)
+                    const float v = a.mu * *vp + y;       // v     (ascent.cpp:68)
+                    const float raw = x + alpha * v;      // raw   (ascent.cpp:69)
+                    if (!isfinite(raw))
+                        atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
+                                  (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
+                    x = raw < -1.f ? -1.f : (raw > 1.f ? 1.f : raw);  // ascent.cpp:73
+                    *xp = x;
+                    *vp = v;
+                }
+                __nv_bfloat16 h, mi, lo;
+                split3(x, h, mi, lo);
+                const int64_t po = static_cast<int64_t>(c) * a.ldp + row;
+                const int64_t ps = static_cast<int64_t>(a.W) * a.ldp;
+                a.planes_out[po] = h;
+                a.planes_out[ps + po] = mi;
+                a.planes_out[2 * ps + po] = lo;
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(N));
+    }
+}
+
+// fp32 [n][ld] (node-major) -> member-major [W][n] fp32 + three bf16 planes
+__global__ void k_to_member_major(const float* __restrict__ X, int64_t ld, int n, int W, float* __restrict__ Xm,
+                                  float* __restrict__ Vm, int ldx, __nv_bfloat16* __restrict__ P, int ldp) {
+    __shared__ float tile[32][33];
+    const int v0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int v = v0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (v < n && c < W) ? X[static_cast<int64_t>(v) * ld + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, v = v0 + threadIdx.x;
+        if (c < W && v < n) {
+            const float x = tile[threadIdx.x][i];
+            Xm[static_cast<int64_t>(c) * ldx + v] = x;
+            Vm[static_cast<int64_t>(c) * ldx + v] = 0.f;
+            __nv_bfloat16 h, m, l;
+            split3(x, h, m, l);
+            const int64_t po = static_cast<int64_t>(c) * ldp + v, ps = static_cast<int64_t>(W) * ldp;
+            P[po] = h;
+            P[ps + po] = m;
+            P[2 * ps + po] = l;
+        }
+    }
+}
+
+__global__ void k_from_member_major(const float* __restrict__ Xm, int ldx, int n, int W, float* __restrict__ X,
+                                    int64_t ld) {
+    __shared__ float tile[32][33];
+    const int v0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, v = v0 + threadIdx.x;
+        tile[i][threadIdx.x] = (c < W && v < n) ? Xm[static_cast<int64_t>(c) * ldx + v] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int v = v0 + i, c = c0 + threadIdx.x;
+        if (v < n && c < W) X[static_cast<int64_t>(v) * ld + c] = tile[threadIdx.x][i];
+    }
+}
+
+// dense bf16 adjacency from CSR: A[v][u] = 1 for every stored neighbour
+__global__ void k_scatter_adjacency(const int* __restrict__ row_ptr, const int* __restrict__ col, int n,
+                                    __nv_bfloat16* __restrict__ A, int64_t lda) {
+    const __nv_bfloat16 one = __float2bfloat16(1.f);
+    for (int v = blockIdx.x; v < n; v += gridDim.x)
+        for (int k = row_ptr[v] + threadIdx.x; k < row_ptr[v + 1]; k += blockDim.x)
+            A[static_cast<int64_t>(v) * lda + col[k]] = one;
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiled>(p);
+    }();
+    return fn;
+}
+
+void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch_elems,
+              uint32_t box_inner, uint32_t box_rows) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) throw Failure{5, "cuTensorMapEncodeTiled unavailable"};
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {pitch_elems * 2};
+    const cuuint32_t box[2] = {box_inner, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Failure{4, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r))};
+}
+
+template <int N>
+void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, const DenseArgs& a, cudaStream_t s) {
+    constexpr int smem = kStages * (kATileBytes + 3 * N * kBK * 2) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dense_step<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    count_launch();
+    k_dense_step<N><<<(a.n + kBM - 1) / kBM, 192, smem, s>>>(mA, mP, a);
+}
+
+}  // namespace
+
+size_t dense_adjacency_bytes(int n) {
+    const int64_t lda = (static_cast<int64_t>(n) + 7) / 8 * 8;
+    return static_cast<size_t>(lda) * n * 2;
+}
+
+void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s) {
+    const int64_t lda = (static_cast<int64_t>(g.n) + 7) / 8 * 8;
+    cuda_check(cudaMemsetAsync(A, 0, dense_adjacency_bytes(g.n), s), "memset(A)");
+    count_launch();
+    k_scatter_adjacency<<<std::min(g.n, 148 * 16), 256, 0, s>>>(g.row_ptr, g.col, g.n,
+                                                                  static_cast<__nv_bfloat16*>(A), lda);
+}
+
+int dense_ldp(int n) { return (n + 7) / 8 * 8; }
+
+// Dense T loop: X0 in node-major [n][ld] (from the batch init), result written back there.
+void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
+                          int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
+                          const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
+                          void* planes, cudaStream_t s, int col_base) {
+    const int n = g.n;
+    const int ldp = dense_ldp(n);
+    const int ldx = ldp;
+    __nv_bfloat16* P = static_cast<__nv_bfloat16*>(planes);
+    __nv_bfloat16* Pbuf[2] = {P, P + static_cast<size_t>(3) * W * ldp};
+    const dim3 tg((n + 31) / 32, (W + 31) / 32);
+    count_launch();
+    k_to_member_major<<<tg, dim3(32, 8), 0, s>>>(X_nodemajor_in, ld, n, W, Xm, Vm, ldx, Pbuf[0], ldp);
+    const int64_t lda = (static_cast<int64_t>(n) + 7) / 8 * 8;
+    // UMMA N (and the plane TMA box height) = W rounded up to 64 / 128 / 256; the extra
+    // columns read the next plane's rows (or OOB zeros) and are never written back
+    const int NB = W <= 64 ? 64 : (W <= 128 ? 128 : 256);
+    CUtensorMap mA, mP[2];
+    make_map(&mA, A, static_cast<uint64_t>(n), static_cast<uint64_t>(n), static_cast<uint64_t>(lda), kBK, kBM);
+    for (int b = 0; b < 2; ++b)
+        make_map(&mP[b], Pbuf[b], static_cast<uint64_t>(n), static_cast<uint64_t>(3) * W, static_cast<uint64_t>(ldp),
+                 kBK, static_cast<uint32_t>(NB));
+    DenseArgs a{};
+    a.deg = g.deg32;
+    a.X = Xm;
+    a.V = Vm;
+    a.n = n;
+    a.ldx = ldx;
+    a.ldp = ldp;
+    a.W = W;
+    a.l = l;
+    a.mu = mu;
+    a.alpha_uniform = alpha_u;
+    a.alpha = alpha_arr;
+    a.tlim = tlim_arr;
+    a.err = err;
+    a.err_seg = err_seg;
+    a.col_base = col_base;
+    for (int64_t it = 0; it < iters; ++it) {
+        a.it = static_cast<int>(it);
+        a.planes_out = Pbuf[(it + 1) & 1];
+        const CUtensorMap& mp = mP[it & 1];
+        if (NB == 64)
+            launch_dense_n<64>(mA, mp, a, s);
+        else if (NB == 128)
+            launch_dense_n<128>(mA, mp, a, s);
+        else
+            launch_dense_n<256>(mA, mp, a, s);
+    }
+    count_launch();
+    k_from_member_major<<<tg, dim3(32, 8), 0, s>>>(Xm, ldx, n, W, X_nodemajor_out, ld);
+}
+
+}  // namespace lcb

@@ -57,6 +57,7 @@ struct DevGraph {
     int* res_heavy = nullptr;     // [heavy][2] absolute word offset, degree
     int res_nheavy = 0;
     uint16_t* res_col = nullptr;  // [padded nnz]
+    void* dense_A = nullptr;      // bf16 [n][roundup(n,8)] adjacency for the tensor-core path (dense graphs)
     int* res_perm = nullptr;      // [n] new row -> original row (== order)
     std::vector<int64_t> h_off;
     std::vector<uint32_t> h_adj;
@@ -119,6 +120,15 @@ struct ResidentArgs {
     int err_seg;             // members per error slot (0: one slot)
 };
 bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K);
+
+// dense tensor-core path (lcb_dense.cu), fp32 iterate, W <= 256
+size_t dense_adjacency_bytes(int n);
+int dense_ldp(int n);
+void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s);
+void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
+                          int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
+                          const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
+                          void* planes, cudaStream_t s, int col_base);
 void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
 
 template <typename T>

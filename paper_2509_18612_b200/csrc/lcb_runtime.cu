@@ -163,6 +163,8 @@ void free_graph(DevGraph& g) {
     cudaFree(g.res_chunk);
     cudaFree(g.res_heavy);
     g.res_heavy = nullptr;
+    cudaFree(g.dense_A);
+    g.dense_A = nullptr;
     cudaFree(g.res_col);
     g.res_info = nullptr;
     g.row_ptr = g.col = g.order = g.res_chunk = nullptr;
@@ -227,6 +229,20 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
 
     g.res_perm = g.order;
+    {
+        // dense tensor-core path: graphs with >= 5% density (config 3), when A fits comfortably
+        const char* e = std::getenv("LCB_DENSE");
+        const int mode = e ? std::atoi(e) : -1;
+        const double density = n > 1 ? static_cast<double>(nnz) / (static_cast<double>(n) * (n - 1)) : 0.0;
+        size_t freeb = 0, totalb = 0;
+        cudaMemGetInfo(&freeb, &totalb);
+        const bool fits = dense_adjacency_bytes(static_cast<int>(n)) < freeb / 3;
+        if (mode != 0 && fits && n >= 256 && (mode == 1 || (density >= 0.05 && n >= 4096))) {
+            CK(cudaMalloc(&g.dense_A, dense_adjacency_bytes(static_cast<int>(n))));
+            build_dense_adjacency(g, g.dense_A, 0);
+            CK(cudaDeviceSynchronize());
+        }
+    }
     if (static_cast<int>(n) <= kResidentMaxRows) {
         // relabelled CSR for the member-resident kernel: new id = rank in `order`,
         // each list padded to a multiple of 4 with the zero sentinel row n; per-row
@@ -358,6 +374,8 @@ struct Work {
     DBuf<uint64_t> mkeys, colkeys;
     DBuf<double> mean, dtrace, hostbatch;
     DBuf<int8_t> sign;
+    DBuf<float> dXm, dVm;        // dense path: member-major iterate / velocity of one column chunk
+    DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes
     DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
     unsigned long long* h_keys = nullptr;  // pinned
     uint32_t* h_flags = nullptr;
@@ -368,7 +386,7 @@ struct Work {
     double step_bytes = 0.0;
     int64_t node_updates = 0;
     int64_t resident_iters = 0;  // iterations executed by the member-resident kernel
-    double kstats[6] = {0, 0, 0, 0, 0, 0};  // K1 {ms, launches, bytes}, K2 {ms, launches, bytes}
+    double kstats[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // K1 / K2 {ms, launches, bytes}, K3 {ms, launches, flops}
 
     explicit Work(int dev) : device(dev) {
         CK(cudaSetDevice(dev));
@@ -508,6 +526,41 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     IterResult r;
     int K = 0;
     const bool resident_enabled = true;
+    if constexpr (std::is_same_v<T, float>) {
+        if (g.dense_A && !trace_host && !ee && iters > 0 && iters <= 0x7fffffff) {
+            // K3: dense adjacency on the tensor cores, column chunks of <= 256
+            CK(cudaEventRecord(w.ev0, w.st));
+            const int ldp = dense_ldp(g.n);
+            for (int c0 = 0; c0 < W; c0 += 256) {
+                const int Wc = std::min(256, W - c0);
+                float* Xm = w.dXm.ensure(static_cast<size_t>(Wc) * ldp);
+                float* Vm = w.dVm.ensure(static_cast<size_t>(Wc) * ldp);
+                void* P = w.dplanes.ensure(static_cast<size_t>(6) * Wc * ldp);
+                // tlim/alpha are per member; chunk boundaries are member-aligned when 256 % l == 0
+                run_dense_iterations(g, g.dense_A, w.X[0].p + c0, w.X[1].p + c0, w.ld, Wc, l, iters, alpha_u,
+                                     alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0);
+            }
+            CK(cudaEventRecord(w.ev1, w.st));
+            CK(cudaGetLastError());
+            d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
+            CK(cudaStreamSynchronize(w.st));
+            r.err = w.h_keys[0];
+            r.errs.assign(w.h_keys, w.h_keys + err_slots);
+            r.iters = iters;
+            r.final_buf = 1;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+            w.step_ms += ms;
+            w.step_launches += iters * ((W + 255) / 256);
+            const double bytes = static_cast<double>(iters) * (16.0 * g.n * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
+            w.step_bytes += bytes;
+            w.kstats[6] += ms;
+            w.kstats[7] += static_cast<double>(iters * ((W + 255) / 256));
+            w.kstats[8] += 2.0 * static_cast<double>(g.n) * g.n * W * iters;  // algorithmic GEMM flops
+            w.node_updates += iters * static_cast<int64_t>(g.n) * W;
+            return r;
+        }
+    }
     if (resident_enabled && !trace_host && g.res_info && iters > 0 && resident_preferred(g, W, sizeof(T)) && iters <= 0x7fffffff &&
         resident_fits(g.n, W, l, ee, static_cast<int>(sizeof(T)), K)) {
         // K2: all iterations in one launch, state resident in SMEM

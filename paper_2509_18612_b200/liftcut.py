@@ -764,7 +764,7 @@ class SolveOutcome:
     node_updates: int = 0
     step_bytes: float = 0.0
     solve_ms: float = 0.0
-    kernel_stats: dict = field(default_factory=dict)  # {"k_step"|"k_resident": (ms, launches, bytes)}
+    kernel_stats: dict = field(default_factory=dict)  # name -> (ms, launches, bytes | flops for k_dense_step)
 
 
 @dataclass
@@ -784,7 +784,7 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
     z = np.zeros(g.node_count(), dtype=np.uint8)
     bt, pt, st = (_abi.BatchTrace * cap)(), (_abi.PhaseTrace * cap)(), (_abi.SearchTrace * cap)()
     step_ms, step_bytes, solve_ms = C.c_double(0), C.c_double(0), C.c_double(0)
-    kst = (C.c_double * 6)()
+    kst = (C.c_double * 9)()
     launches, nupd = C.c_int64(0), C.c_int64(0)
     ro = _abi.RunOpts(precision=default_precision() if opts.precision is None else opts.precision,
                       host_init=opts.host_init, batched_search=int(opts.batched_search),
@@ -815,7 +815,8 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
         stage_times=StageTimes(out.init_s, out.ascent_s, out.rounding_s, out.search_s),
         batches_run=out.batches_run, step_ms=step_ms.value, step_launches=launches.value,
         node_updates=nupd.value, step_bytes=step_bytes.value, solve_ms=solve_ms.value,
-        kernel_stats={"k_step": tuple(kst[0:3]), "k_resident": tuple(kst[3:6])})
+        kernel_stats={"k_step": tuple(kst[0:3]), "k_resident": tuple(kst[3:6]),
+                      "k_dense_step": tuple(kst[6:9])})
 
 
 def counters():

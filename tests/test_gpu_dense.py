@@ -1,0 +1,55 @@
+"""K3 dense tensor-core path (tcgen05 + TMA, bf16 hi/mid/lo planes, fp32 TMEM
+accumulation) against the fp64 oracle.  Runs in a subprocess with LCB_DENSE=1 so the
+small test graphs take the dense path."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CODE = r"""
+import json, sys, numpy as np
+import oracle as O
+from paper_2509_18612_b200 import liftcut as lc, LCB_FP32
+res = {}
+cg = O.generate_er(600, 0.5, 3)
+g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+rng = np.random.default_rng(0)
+for (l, B) in [(1, 64), (1, 256), (2, 100), (1, 320)]:
+    x = rng.choice([-1e-4, 1e-4], B * l * cg.n) + rng.normal(0, 9e-5, B * l * cg.n)
+    worst = {}
+    for T in (1, 4, 10):
+        want, _ = O.ascend(cg, x, l, B, 0.01, T, 0.9, False)
+        s = lc.DenseState(cg.n, l, B); s.values[:] = x
+        lc.ascend(g, s, lc.AscentParams(0.01, T, 0.9, False), precision=LCB_FP32)
+        e = 0.0
+        for j in range(B):
+            a, b = s.values[j*l*cg.n:(j+1)*l*cg.n], want[j*l*cg.n:(j+1)*l*cg.n]
+            e = max(e, float(np.max(np.abs(a - b)) / np.max(np.abs(b))))
+        worst[T] = e
+    T = 200
+    want, _ = O.ascend(cg, x, l, B, 0.01, T, 0.9, False)
+    s = lc.DenseState(cg.n, l, B); s.values[:] = x
+    lc.ascend(g, s, lc.AscentParams(0.01, T, 0.9, False), precision=LCB_FP32)
+    c32, _, _, _ = lc.round_cut_batch(g, s, lifted=l > 1)
+    sw = lc.DenseState(cg.n, l, B); sw.values[:] = want
+    c64, _, _, _ = lc.round_cut_batch(g, sw, lifted=l > 1)
+    res[f"{l}x{B}"] = dict(err=worst, same=float(np.mean(c32 == c64)), d=int(abs(c32.max() - c64.max())))
+print("RESULT" + json.dumps(res))
+"""
+
+
+def test_dense_tensor_core_path_matches_oracle():
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", CODE], cwd=root, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "LCB_DENSE": "1"})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    res = json.loads(r.stdout.split("RESULT")[1])
+    print(res)
+    for k, v in res.items():
+        for T, e in v["err"].items():
+            assert e <= 1e-5, (k, T, e)  # fp32 contract
+        assert v["same"] >= 0.97 and v["d"] <= 2, (k, v)

@@ -87,6 +87,7 @@ struct StepArgs {
     int members;
     unsigned long long* err;    // min over (member << 32 | iteration)
     int err_seg;                // members per error slot (0: one slot) — batched search
+    int col_base;               // batch column of x_in[0] (L2-panel column chunks)
     T mu;
     T alpha_uniform;            // used when alpha == nullptr
     int it;

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                     int m = 0;
                     if constexpr (GEN) {
                         if (act) {
-                            m = colx / a.l;
+                            m = (a.col_base + colx) / a.l;
                             if (a.tlim) act = a.it < __ldg(a.tlim + m);
                             if constexpr (EE) {
                                 if (act && a.it > 0) act = ex_continue(__ldcg(a.flags_prev + m));
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                             if (a.alpha) alpha = __ldg(a.alpha + m);
                         }
                     } else {
-                        m = colx / a.l;
+                        m = (a.col_base + colx) / a.l;
                     }
                     if (act) {
                         const T y = rsub(rmul(dg, x), el(acc[s], e));     // Lx  (graph.cpp:120)
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             const uint32_t b = sbits[i];
             const int colx = group * SPAN + i;
             if (b && colx < a.W) {
-                const int m = colx / a.l;
+                const int m = (a.col_base + colx) / a.l;
                 const uint32_t f = __ldcg(a.flags_cur + m);
                 if ((f & b) != b) atomicOr(a.flags_cur + m, b);
             }
@@ -227,7 +227,7 @@ void dispatch_s(const StepArgs<T>& a, int S, cudaStream_t st) {
     auto go = [&](auto sconst) {
         constexpr int SS = decltype(sconst)::value;
         constexpr int SPAN = 32 * SS * E;
-        const int groups = static_cast<int>((a.ld + SPAN - 1) / SPAN);
+        const int groups = (a.W + SPAN - 1) / SPAN;  // slabs covering the live columns
         const dim3 grid(static_cast<unsigned>(rows_blocks) * groups);
         count_launch();
         k_step<T, SS, GEN, EE, MODE><<<grid, kWarps * 32, 0, st>>>(a, groups);

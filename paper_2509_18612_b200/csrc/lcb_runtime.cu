@@ -609,6 +609,60 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         w.resident_iters += iters;
         return r;
     }
+    // L2-panel member chunking (SURVEY 7 "throughput kernels"): when the iterate is far
+    // larger than L2, run all T iterations for one 128-column slab at a time so the slab's
+    // x-panel (read deg times per iteration by the gathers) stays L2-resident.
+    {
+        static const int64_t l2 = [] {
+            int v = 0;
+            cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
+            return static_cast<int64_t>(v > 0 ? v : (126 << 20));
+        }();
+        static const int chunk_mode = [] {
+            const char* e = std::getenv("LCB_CHUNK");
+            return e ? std::atoi(e) : -1;
+        }();
+        const int span = step_span<T>(W);
+        const int64_t panel = static_cast<int64_t>(g.n) * W * static_cast<int64_t>(sizeof(T));
+        const int64_t slab_panel = static_cast<int64_t>(g.n) * span * static_cast<int64_t>(sizeof(T));
+        const bool want = chunk_mode == 1 || (chunk_mode != 0 && panel > l2 && slab_panel * 3 <= l2);
+        if (want && !ee && !trace_host && W > span) {
+            CK(cudaEventRecord(w.ev0, w.st));
+            for (int c0 = 0; c0 < W; c0 += span) {
+                StepArgs<T> b = a;
+                b.W = std::min(span, W - c0);
+                b.col_base = c0;
+                b.vel = w.V.p + c0;
+                for (int64_t i = 0; i < iters; ++i) {
+                    b.x_in = w.X[i & 1].p + c0;
+                    b.x_out = w.X[(i + 1) & 1].p + c0;
+                    b.it = static_cast<int>(i);
+                    launch_step<T>(b, false, MODE_STEP, w.st);
+                }
+            }
+            CK(cudaEventRecord(w.ev1, w.st));
+            CK(cudaGetLastError());
+            d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
+            CK(cudaStreamSynchronize(w.st));
+            r.err = w.h_keys[0];
+            r.errs.assign(w.h_keys, w.h_keys + err_slots);
+            r.iters = iters;
+            r.final_buf = static_cast<int>(iters & 1);
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+            const int chunks = (W + span - 1) / span;
+            w.step_ms += ms;
+            w.step_launches += iters * chunks;
+            const double bytes = static_cast<double>(iters) *
+                                 (4.0 * sizeof(T) * static_cast<double>(g.n) * W + chunks * (4.0 * g.nnz + 4.0 * (g.n + 1)));
+            w.step_bytes += bytes;
+            w.kstats[0] += ms;
+            w.kstats[1] += static_cast<double>(iters * chunks);
+            w.kstats[2] += bytes;
+            w.node_updates += iters * static_cast<int64_t>(g.n) * W;
+            return r;
+        }
+    }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;
     for (; it < iters; ++it) {

@@ -372,3 +372,28 @@ def test_batched_search_rounds_match_sequential_and_reference(golden):
     w = O.solve(cg, O.default_config(batch_size=64, num_batches=2, iterations=60, has_search=1, t_lower=20,
                                      t_upper=80, e_lower=-3.0, e_upper=-1.0, population_size=6, rounds=3), 11)
     assert b.best.cut_value == w.cut_value and b.best.assignment.tolist() == w.assignment.tolist()
+
+
+def test_l2_panel_chunked_driver_bitwise(tmp_path):
+    """The column-chunked T loop (forced with LCB_CHUNK=1) gives the same fp64 bits."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, oracle as O\n"
+        "from paper_2509_18612_b200 import liftcut as lc, LCB_FP64\n"
+        "cg = O.generate_er(20000, 0.0004, 5)\n"
+        "g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)\n"
+        "rng = np.random.default_rng(1)\n"
+        "for l, B in ((1, 80), (2, 41)):\n"
+        "    x = rng.uniform(-1e-3, 1e-3, B * l * cg.n)\n"
+        "    want, _ = O.ascend(cg, x, l, B, 0.05, 12, 0.9, False)\n"
+        "    s = lc.DenseState(cg.n, l, B); s.values[:] = x\n"
+        "    lc.ascend(g, s, lc.AscentParams(0.05, 12, 0.9, False), precision=LCB_FP64)\n"
+        "    assert np.array_equal(s.values, want), (l, B)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "LCB_CHUNK": "1", "LCB_RESIDENT": "0"})
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-2000:]

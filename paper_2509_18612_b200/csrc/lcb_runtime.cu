@@ -494,7 +494,8 @@ struct IterResult {
 template <class T>
 IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int l, int64_t iters,
                           T alpha_u, const T* alpha_arr, const int* tlim_arr, T mu, bool ee,
-                          double* trace_host /* [iters][members] or null */, int err_seg = 0) {
+                          double* trace_host /* [iters][members] or null */, int err_seg = 0,
+                          const std::vector<int64_t>* seg_iters = nullptr /* per err segment, descending */) {
     const int err_slots = err_seg > 0 ? (members + err_seg - 1) / err_seg : 1;
     StepArgs<T> a{};
     a.row_ptr = g.row_ptr;
@@ -537,7 +538,12 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                 float* Vm = w.dVm.ensure(static_cast<size_t>(Wc) * ldp);
                 void* P = w.dplanes.ensure(static_cast<size_t>(6) * Wc * ldp);
                 // tlim/alpha are per member; chunk boundaries are member-aligned when 256 % l == 0
-                run_dense_iterations(g, g.dense_A, w.X[0].p + c0, w.X[1].p + c0, w.ld, Wc, l, iters, alpha_u,
+                int64_t chunk_iters = iters;
+                if (seg_iters && err_seg > 0) {  // segments in descending T: the chunk's first one is the longest
+                    const size_t seg = static_cast<size_t>(c0 / (err_seg * l));
+                    if (seg < seg_iters->size()) chunk_iters = (*seg_iters)[seg];
+                }
+                run_dense_iterations(g, g.dense_A, w.X[0].p + c0, w.X[1].p + c0, w.ld, Wc, l, chunk_iters, alpha_u,
                                      alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0);
             }
             CK(cudaEventRecord(w.ev1, w.st));
@@ -665,10 +671,16 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;
+    const int seg_cols = err_seg * l;
+    size_t live_segs = seg_iters ? seg_iters->size() : 0;
     for (; it < iters; ++it) {
         a.x_in = w.X[it & 1].p;
         a.x_out = w.X[(it + 1) & 1].p;
         a.it = static_cast<int>(it);
+        if (seg_iters) {  // candidates laid out by descending T: launch only the live prefix
+            while (live_segs > 0 && (*seg_iters)[live_segs - 1] <= it) --live_segs;
+            a.W = std::min(W, static_cast<int>(live_segs) * seg_cols);
+        }
         if (ee) {
             a.flags_prev = F + ((it + 2) % 3) * members;
             a.flags_cur = F + (it % 3) * members;
@@ -696,6 +708,18 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             if (!any && !tlim_arr) {
                 ++it;
                 break;
+            }
+        }
+    }
+    if (seg_iters) {
+        // a segment that stopped at T_s left its final iterate in X[T_s & 1]
+        for (size_t sgi = 0; sgi < seg_iters->size(); ++sgi) {
+            const int64_t ts = (*seg_iters)[sgi];
+            if (ts < it && ((ts ^ it) & 1)) {
+                const size_t pitch = sizeof(T) * static_cast<size_t>(w.ld);
+                CK(cudaMemcpy2DAsync(w.X[it & 1].p + sgi * seg_cols, pitch, w.X[ts & 1].p + sgi * seg_cols, pitch,
+                                     sizeof(T) * static_cast<size_t>(seg_cols), static_cast<size_t>(g.n),
+                                     cudaMemcpyDeviceToDevice, w.st));
             }
         }
     }
@@ -934,6 +958,7 @@ struct Solver {
     struct MultiRes {
         std::vector<BatchRes> res;
         std::vector<bool> numeric;
+        std::vector<int> seg_of;  // candidate -> batch segment
         unsigned long long* d_keys = nullptr;
         uint32_t* Z = nullptr;
     };
@@ -947,18 +972,27 @@ struct Solver {
         const int members = static_cast<int>(B) * K;
         const int W = members * l;
         w.shape(n, W);
+        // segment order: candidates by descending T (stable), so finished candidates are a
+        // suffix of the batch and the launches shrink as they finish
+        std::vector<int> order(static_cast<size_t>(K));
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int x, int y) { return cs[x]->iterations > cs[y]->iterations; });
         std::vector<uint64_t> mk;
-        for (int k = 0; k < K; ++k) member_keys(serial0 + k, mk);
+        for (int sgi = 0; sgi < K; ++sgi) member_keys(serial0 + order[sgi], mk);
         init_batch(l, nullptr, bits, mk, std::sqrt(eta_eff));
         std::vector<T> alpha(static_cast<size_t>(members));
         std::vector<int> tlim(static_cast<size_t>(members));
+        std::vector<int64_t> seg_iters(static_cast<size_t>(K));
         int64_t tmax = 0, upd = 0;
-        for (int k = 0; k < K; ++k) {
-            tmax = std::max(tmax, cs[k]->iterations);
-            upd += cs[k]->iterations;
+        for (int sgi = 0; sgi < K; ++sgi) {
+            const Cand& c = *cs[order[sgi]];
+            seg_iters[sgi] = c.iterations;
+            tmax = std::max(tmax, c.iterations);
+            upd += c.iterations;
             for (int64_t j = 0; j < B; ++j) {
-                alpha[static_cast<size_t>(k * B + j)] = static_cast<T>(cs[k]->alpha());
-                tlim[static_cast<size_t>(k * B + j)] = static_cast<int>(cs[k]->iterations);
+                alpha[static_cast<size_t>(sgi * B + j)] = static_cast<T>(c.alpha());
+                tlim[static_cast<size_t>(sgi * B + j)] = static_cast<int>(c.iterations);
             }
         }
         T* da = w.alpha.ensure(alpha.size());
@@ -967,7 +1001,7 @@ struct Solver {
         h2d(dt, tlim.data(), sizeof(int) * tlim.size(), w.st);
         const int64_t before = w.node_updates;
         IterResult ir = run_iterations<T>(g, w, W, members, l, tmax, T(0), da, dt, static_cast<T>(mu), ee,
-                                          nullptr, static_cast<int>(B));
+                                          nullptr, static_cast<int>(B), &seg_iters);
         sync_errors(ir);
         w.node_updates = before + upd * static_cast<int64_t>(n) * B * l;  // active updates only
         MultiRes out;
@@ -985,22 +1019,26 @@ struct Solver {
         d2h(w.h_keys, out.d_keys, sizeof(unsigned long long) * K, w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
+        out.seg_of.assign(static_cast<size_t>(K), 0);
+        for (int sgi = 0; sgi < K; ++sgi) out.seg_of[static_cast<size_t>(order[sgi])] = sgi;
         for (int k = 0; k < K; ++k) {
-            const unsigned long long key = w.h_keys[k];
+            const int sgi = out.seg_of[static_cast<size_t>(k)];
+            const unsigned long long key = w.h_keys[sgi];
             BatchRes r;
             r.cut = static_cast<int64_t>(key >> 32);
             r.member = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull));
             r.serial = serial0 + k;
             out.res.push_back(r);
-            out.numeric.push_back(k < static_cast<int>(ir.errs.size()) && ir.errs[k] != ~0ull);
+            out.numeric.push_back(sgi < static_cast<int>(ir.errs.size()) && ir.errs[sgi] != ~0ull);
         }
         return out;
     }
 
     // winner bits of segment k of the last multi batch -> w.win
     void multi_winner(const MultiRes& m, int k) {
-        launch_extract_winner(m.Z, g.n, m.d_keys + k, member_base, static_cast<int>(B) * (k + 1), w.win.p, w.st,
-                              static_cast<int>(B) * k);
+        const int sgi = m.seg_of[static_cast<size_t>(k)];
+        launch_extract_winner(m.Z, g.n, m.d_keys + sgi, member_base, static_cast<int>(B) * (sgi + 1), w.win.p, w.st,
+                              static_cast<int>(B) * sgi);
         if (comm && comm->comm)
             nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
                                         comm->comm, w.st),

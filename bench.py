@@ -271,7 +271,9 @@ def run_b200(args):
         comm = Comm.from_torch(local)
     prec = LCB_FP32 if args.precision == "fp32" else LCB_FP64
     g, cfg, desc = workload(args.config, world, args.precision)
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=comm, batched_search=True)
+    # batched search rounds measured slower on config 5 (B=256 already fills the GPU; see
+    # profiles/round1_kernel_ab.md), so the bench keeps the sequential evolve() order
+    opts = lc.RunOptions(precision=prec, host_init=0, comm=comm, batched_search=False)
     solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[int(cfg.algorithm)]
     g.handle(local)  # inputs resident in HBM before timing
 

@@ -78,6 +78,9 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
     return as_f2(r);
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 // 8-byte shared load at a 32-bit shared-window byte address
 __device__ __forceinline__ float2 lds2(uint32_t addr) {
     float2 v;
@@ -126,6 +129,47 @@ __device__ __forceinline__ void gather4(float2& acc, const float2* cur, uint2 w)
     acc = add2(acc, g1);
     acc = add2(acc, g2);
     acc = add2(acc, g3);
+}
+
+template <typename VT>
+__device__ __forceinline__ VT ldsv(uint32_t addr);
+template <>
+__device__ __forceinline__ float ldsv<float>(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+template <>
+__device__ __forceinline__ float2 ldsv<float2>(uint32_t addr) {
+    return lds2(addr);
+}
+template <>
+__device__ __forceinline__ double ldsv<double>(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void stsv(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void stsv(uint32_t addr, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void stsv(uint32_t addr, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+// four neighbours (CSR order) of a packed uint16 column word, slab base in the shared window
+template <typename VT>
+__device__ __forceinline__ void gather4s(VT& acc, uint32_t base, uint2 w) {
+    constexpr uint32_t sz = sizeof(VT);
+    const VT g0 = ldsv<VT>(base + (w.x & 0xffffu) * sz);
+    const VT g1 = ldsv<VT>(base + (w.x >> 16) * sz);
+    const VT g2 = ldsv<VT>(base + (w.y & 0xffffu) * sz);
+    const VT g3 = ldsv<VT>(base + (w.y >> 16) * sz);
+    addto(acc, g0);
+    addto(acc, g1);
+    addto(acc, g2);
+    addto(acc, g3);
 }
 
 template <typename VT>
@@ -281,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int i = j * kThreads + ((j & 1) ? kThreads - 1 - tid : tid);
-        info[j] = H + i < n ? __ldg(a.rowinfo + i) : 0u;
+        info[j] = H + i < n ? __ldg(a.rowinfo + i) : 0u;  // (absolute col4 word << 8) | degree
         vel[j] = zero_v<VT>();
     }
     // heavy rows: COOP -> lane (sub*8 + hs) owns heavy row hs*128 + snake(warp*4+sub); else thread tid owns row tid
@@ -339,38 +383,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
             nxt[tid] = xo;
         }
 
-        // ---- light rows, one row ahead prefetch of the first column word
-        uint2 pre = make_uint2(0u, 0u);
-        {
-            const int i0 = tid;
-            if (H + i0 < n) pre = __ldg(col4 + __ldg(a.chunk_base) + (info[0] >> 16));
-        }
+        // ---- light rows: packed (absolute 4-column word << 8 | degree) per row in a register,
+        // shared-window byte addresses formed once per iteration
+        const uint32_t cur_b = smem_u32(cur), nxt_b = smem_u32(nxt);
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            const int i = j * kThreads + ((j & 1) ? kThreads - 1 - tid : tid);
-            const int r = H + i;
-            const uint2 w0 = pre;
-            if (j + 1 < RPT) {
-                const int i1 = (j + 1) * kThreads + (((j + 1) & 1) ? kThreads - 1 - tid : tid);
-                if (H + i1 < n) pre = __ldg(col4 + __ldg(a.chunk_base + j + 1) + (info[j + 1] >> 16));
-            }
+            const int r = H + j * kThreads + ((j & 1) ? kThreads - 1 - tid : tid);
             if (r < n) {
-                const int dj = static_cast<int>(info[j] & 0xffffu);
+                const uint32_t pk = info[j];
+                const int dj = static_cast<int>(pk & 0xffu);
                 const int words = (dj + 3) >> 2;
-                const uint2* cp = col4 + __ldg(a.chunk_base + j) + (info[j] >> 16);
+                const uint2* cp = col4 + (pk >> 8);
                 VT acc = zero_v<VT>();
-                if (words > 0) gather4(acc, cur, w0);  // isolated rows own no column word
-                int q = 1;
+                int q = 0;
                 for (; q + 2 <= words; q += 2) {
                     const uint2 w1 = __ldg(cp + q);
                     const uint2 w2 = __ldg(cp + q + 1);
-                    gather4(acc, cur, w1);
-                    gather4(acc, cur, w2);
+                    gather4s(acc, cur_b, w1);
+                    gather4s(acc, cur_b, w2);
                 }
-                if (q < words) gather4(acc, cur, __ldg(cp + q));
+                if (q < words) gather4s(acc, cur_b, __ldg(cp + q));
                 VT xo;
-                row_update_any<T, VT, K, EE>(cur[r], acc, vel[j], xo, dj, act, alpha_k, mu, mem, it, bits, errp, packed);
-                nxt[r] = xo;
+                row_update_any<T, VT, K, EE>(ldsv<VT>(cur_b + static_cast<uint32_t>(r) * sizeof(VT)), acc, vel[j], xo,
+                                             dj, act, alpha_k, mu, mem, it, bits, errp, packed);
+                stsv(nxt_b + static_cast<uint32_t>(r) * sizeof(VT), xo);
             }
         }
         if (EE) {

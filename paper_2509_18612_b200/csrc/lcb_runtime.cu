@@ -267,14 +267,14 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             hinfo[2 * h] = static_cast<int>(rrp[h] / 4);
             hinfo[2 * h + 1] = deg[ord[h]];
         }
-        bool packable = rrp[n] / 4 < (int64_t(1) << 31);
+        // light row i: (absolute 4-column word << 8) | degree  (degree <= 255, word < 2^24)
+        bool packable = rrp[n] / 4 < (int64_t(1) << 24);
         for (uint32_t i = 0; i < L && packable; ++i) {
             const uint32_t r = H + i;
             if (i % 1024 == 0) cbase[i / 1024] = static_cast<int>(rrp[r] / 4);
-            const int64_t rel = rrp[r] / 4 - cbase[i / 1024];
             const int d = deg[ord[r]];
-            if (rel >= 65536 || d >= 65536) packable = false;
-            info[i] = (static_cast<uint32_t>(rel) << 16) | static_cast<uint32_t>(d);
+            if (d > 255) packable = false;
+            info[i] = (static_cast<uint32_t>(rrp[r] / 4) << 8) | static_cast<uint32_t>(d);
         }
         if (packable) {
             std::vector<uint16_t> rcol(static_cast<size_t>(std::max<int64_t>(rrp[n], 4)), static_cast<uint16_t>(n));

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "lcb_internal.h"
@@ -143,7 +144,40 @@ struct DenseArgs {
     unsigned long long* err;
     int err_seg;
     int it;
+    int tile_base;           // first M-tile of this launch
+    int k_split;             // K pieces per tile (1: whole K, fused epilogue)
+    float* partial;          // k_split > 1: fp32 partial sums [block][N][128]
 };
+
+// Fused heavy-ball step for one (row, column) given Ax (ascent.cpp:66-77) + plane split.
+__device__ __forceinline__ void finish_element(const DenseArgs& a, int row, int c, float ax, float dg) {
+    const int m = (a.col_base + c) / a.l;
+    bool act = true;
+    float alpha = a.alpha_uniform;
+    if (a.tlim) act = a.it < __ldg(a.tlim + m);
+    if (a.alpha) alpha = __ldg(a.alpha + m);
+    float* xp = a.X + static_cast<int64_t>(c) * a.ldx + row;
+    float* vp = a.V + static_cast<int64_t>(c) * a.ldx + row;
+    float x = *xp;
+    if (act) {
+        const float y = dg * x - ax;          // Lx    (graph.cpp:120)
+        const float v = a.mu * *vp + y;       // v     (ascent.cpp:68)
+        const float raw = x + alpha * v;      // raw   (ascent.cpp:69)
+        if (!isfinite(raw))
+            atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
+                      (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
+        x = raw < -1.f ? -1.f : (raw > 1.f ? 1.f : raw);  // ascent.cpp:73
+        *xp = x;
+        *vp = v;
+    }
+    __nv_bfloat16 h, mi, lo;
+    split3(x, h, mi, lo);
+    const int64_t po = static_cast<int64_t>(c) * a.ldp + row;
+    const int64_t ps = static_cast<int64_t>(a.W) * a.ldp;
+    a.planes_out[po] = h;
+    a.planes_out[ps + po] = mi;
+    a.planes_out[2 * ps + po] = lo;
+}
 
 template <int N>
 __global__ void __launch_bounds__(192, 1)
@@ -156,8 +190,12 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * kBM;
-    const int nk = (a.n + kBK - 1) / kBK;
+    const int tile = a.tile_base + static_cast<int>(blockIdx.x) / a.k_split;
+    const int piece = static_cast<int>(blockIdx.x) % a.k_split;
+    const int m0 = tile * kBM;
+    const int nk_all = (a.n + kBK - 1) / kBK;
+    const int kb = piece * nk_all / a.k_split;
+    const int nk = (piece + 1) * nk_all / a.k_split - kb;   // K steps of this block
     // 1024-byte aligned ring
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
 
@@ -189,10 +227,10 @@ __global__ void __launch_bounds__(192, 1)
                 if (k >= kStages) mbar_wait(&empty_bar[s], ((k / kStages) - 1) & 1);
                 uint8_t* st = ring + s * kStageBytes;
                 mbar_expect_tx(&full_bar[s], kStageBytes);
-                tma_load_2d(st, &tmA, &full_bar[s], k * kBK, m0);
+                tma_load_2d(st, &tmA, &full_bar[s], (kb + k) * kBK, m0);
 #pragma unroll
                 for (int p = 0; p < 3; ++p)
-                    tma_load_2d(st + kATileBytes + p * kPlaneTile, &tmP, &full_bar[s], k * kBK, p * a.W);
+                    tma_load_2d(st + kATileBytes + p * kPlaneTile, &tmP, &full_bar[s], (kb + k) * kBK, p * a.W);
             }
         }
     } else if (warp == 1) {
@@ -228,38 +266,17 @@ __global__ void __launch_bounds__(192, 1)
         for (int c0 = 0; c0 < N; c0 += 32) {
             uint32_t r[32];
             tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
+            if (a.k_split > 1) {  // split-K piece: fp32 partial sums, coalesced along rows
+                float* pp = a.partial + static_cast<int64_t>(blockIdx.x) * N * kBM + q * 32 + lane;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) pp[static_cast<int64_t>(c0 + j) * kBM] = __uint_as_float(r[j]);
+                continue;
+            }
             if (!live) continue;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int c = c0 + j;
-                if (c >= a.W) continue;
-                const int m = (a.col_base + c) / a.l;
-                bool act = true;
-                float alpha = a.alpha_uniform;
-                if (a.tlim) act = a.it < __ldg(a.tlim + m);
-                if (a.alpha) alpha = __ldg(a.alpha + m);
-                float* xp = a.X + static_cast<int64_t>(c) * a.ldx + row;
-                float* vp = a.V + static_cast<int64_t>(c) * a.ldx + row;
-                float x = *xp;
-                if (act) {
-                    const float ax = __uint_as_float(r[j]);
-                    const float y = dg * x - ax;          // Lx    (graph.cpp:120)
-                    const float v = a.mu * *vp + y;       // v     (ascent.cpp:68)
-                    const float raw = x + alpha * v;      // raw   (ascent.cpp:69)
-                    if (!isfinite(raw))
-                        atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
-                                  (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
-                    x = raw < -1.f ? -1.f : (raw > 1.f ? 1.f : raw);  // ascent.cpp:73
-                    *xp = x;
-                    *vp = v;
-                }
-                __nv_bfloat16 h, mi, lo;
-                split3(x, h, mi, lo);
-                const int64_t po = static_cast<int64_t>(c) * a.ldp + row;
-                const int64_t ps = static_cast<int64_t>(a.W) * a.ldp;
-                a.planes_out[po] = h;
-                a.planes_out[ps + po] = mi;
-                a.planes_out[2 * ps + po] = lo;
+                if (c < a.W) finish_element(a, row, c, __uint_as_float(r[j]), dg);
             }
         }
         tc_fence_before();
@@ -268,6 +285,22 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(N));
+    }
+}
+
+// split-K tail: sum the pieces of each tail tile in a fixed order, then the fused step
+template <int N>
+__global__ void k_dense_reduce(DenseArgs a) {
+    const int t = blockIdx.y;                         // tail tile index within this launch
+    const int row_in = threadIdx.x;                   // 0..127
+    const int row = (a.tile_base + t) * kBM + row_in;
+    if (row >= a.n) return;
+    const float dg = __ldg(a.deg + row);
+    for (int c = blockIdx.x; c < a.W; c += gridDim.x) {
+        float ax = 0.f;
+        for (int p = 0; p < a.k_split; ++p)
+            ax += a.partial[(static_cast<int64_t>(t) * a.k_split + p) * N * kBM + static_cast<int64_t>(c) * kBM + row_in];
+        finish_element(a, row, c, ax, dg);
     }
 }
 
@@ -352,18 +385,43 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
 }
 
 template <int N>
-void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, const DenseArgs& a, cudaStream_t s) {
+void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, float* partial, cudaStream_t s) {
     constexpr int smem = kStages * (kATileBytes + 3 * N * kBK * 2) + 1024;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_dense_step<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
+    // Wave quantisation: full tiles fill whole waves of the SMs; the remaining tail tiles are
+    // split along K so the tail also fills one wave, reduced in a fixed order afterwards.
+    static const int sms = [] {
+        const char* e = std::getenv("LCB_DENSE_SMS");  // test hook: pretend a smaller wave
+        return e ? std::atoi(e) : num_sms(0);
+    }();
+    const int tiles = (a.n + kBM - 1) / kBM;
+    int tail = tiles % sms;
+    if (tail * 2 > sms || tiles < sms || partial == nullptr) tail = 0;  // tail already fills >= half a wave
+    const int full = tiles - tail;
+    a.tile_base = 0;
+    a.k_split = 1;
+    a.partial = nullptr;
     count_launch();
-    k_dense_step<N><<<(a.n + kBM - 1) / kBM, 192, smem, s>>>(mA, mP, a);
+    k_dense_step<N><<<full, 192, smem, s>>>(mA, mP, a);
+    if (tail > 0) {
+        const int split = std::max(2, sms / tail);
+        a.tile_base = full;
+        a.k_split = split;
+        a.partial = partial;
+        count_launch();
+        k_dense_step<N><<<tail * split, 192, smem, s>>>(mA, mP, a);
+        count_launch();
+        k_dense_reduce<N><<<dim3(std::min(a.W, 64), tail), kBM, 0, s>>>(a);
+    }
 }
 
 }  // namespace
+
+size_t dense_partial_floats() { return static_cast<size_t>(148 * 2) * 256 * kBM; }
 
 size_t dense_adjacency_bytes(int n) {
     const int64_t lda = (static_cast<int64_t>(n) + 7) / 8 * 8;
@@ -384,7 +442,7 @@ int dense_ldp(int n) { return (n + 7) / 8 * 8; }
 void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
                           int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
-                          void* planes, cudaStream_t s, int col_base) {
+                          void* planes, cudaStream_t s, int col_base, float* partial) {
     const int n = g.n;
     const int ldp = dense_ldp(n);
     const int ldx = ldp;
@@ -423,11 +481,11 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
         a.planes_out = Pbuf[(it + 1) & 1];
         const CUtensorMap& mp = mP[it & 1];
         if (NB == 64)
-            launch_dense_n<64>(mA, mp, a, s);
+            launch_dense_n<64>(mA, mp, a, partial, s);
         else if (NB == 128)
-            launch_dense_n<128>(mA, mp, a, s);
+            launch_dense_n<128>(mA, mp, a, partial, s);
         else
-            launch_dense_n<256>(mA, mp, a, s);
+            launch_dense_n<256>(mA, mp, a, partial, s);
     }
     count_launch();
     k_from_member_major<<<tg, dim3(32, 8), 0, s>>>(Xm, ldx, n, W, X_nodemajor_out, ld);

@@ -129,7 +129,8 @@ void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s);
 void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
                           int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
-                          void* planes, cudaStream_t s, int col_base);
+                          void* planes, cudaStream_t s, int col_base, float* partial);
+size_t dense_partial_floats();
 void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
 
 template <typename T>

@@ -75,8 +75,16 @@ __global__ void __launch_bounds__(kWarps * 32)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+#if LCB_GROUP_MAJOR
+    // slab-major block order: all SMs work the same column slab at a time, so the slabs
+    // of hub rows (gathered by many rows) stay in L1
+    const int rows_blocks = (a.n + kWarps - 1) / kWarps;
+    const int group = blockIdx.x / rows_blocks;
+    const int slot = (blockIdx.x % rows_blocks) * kWarps + warp;
+#else
     const int group = blockIdx.x % groups;
     const int slot = (blockIdx.x / groups) * kWarps + warp;
+#endif
 
     if constexpr (EE) {
         for (int i = threadIdx.x; i < SPAN; i += blockDim.x) sbits[i] = 0;

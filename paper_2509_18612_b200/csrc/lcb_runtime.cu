@@ -376,6 +376,7 @@ struct Work {
     DBuf<int8_t> sign;
     DBuf<float> dXm, dVm;        // dense path: member-major iterate / velocity of one column chunk
     DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes
+    DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
     DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
     unsigned long long* h_keys = nullptr;  // pinned
     uint32_t* h_flags = nullptr;
@@ -543,8 +544,9 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                     const size_t seg = static_cast<size_t>(c0 / (err_seg * l));
                     if (seg < seg_iters->size()) chunk_iters = (*seg_iters)[seg];
                 }
+                float* part = w.dpartial.ensure(dense_partial_floats());
                 run_dense_iterations(g, g.dense_A, w.X[0].p + c0, w.X[1].p + c0, w.ld, Wc, l, chunk_iters, alpha_u,
-                                     alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0);
+                                     alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0, part);
             }
             CK(cudaEventRecord(w.ev1, w.st));
             CK(cudaGetLastError());

@@ -48,10 +48,16 @@ print("RESULT" + json.dumps(res))
 """
 
 
-def test_dense_tensor_core_path_matches_oracle():
+@pytest.mark.parametrize("sms", [None, "4"])
+def test_dense_tensor_core_path_matches_oracle(sms):
+    """sms="4": pretend a 4-SM wave so the 5-tile graph exercises the split-K tail
+    (4 full tiles + 1 tail tile in 4 K pieces + fixed-order reduce)."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "LCB_DENSE": "1"}
+    if sms:
+        env["LCB_DENSE_SMS"] = sms
     r = subprocess.run([sys.executable, "-c", CODE], cwd=root, capture_output=True, text=True, timeout=900,
-                       env={**os.environ, "LCB_DENSE": "1"})
+                       env=env)
     assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
     res = json.loads(r.stdout.split("RESULT")[1])
     print(res)

@@ -8,10 +8,10 @@
 // fp32-faithful A·X (executed flops = 3x algorithmic).
 //
 // One CTA per 128-row tile of A (M=128), all N = W (<= 256) columns:
-//   warp 0  TMA producer: A tile [128 x 64] + 3 plane tiles [W x 64] per K step,
-//           128-byte swizzle, 2-stage ring, mbarrier complete_tx;
+//   warp 0  TMA producer: A tile [128 x 32] + 3 plane tiles [N x 32] per K step,
+//           64-byte swizzle, 4-stage ring, mbarrier complete_tx;
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16 x bf16
-//           -> fp32, 12 MMAs of K=16 per K step), tcgen05.commit frees ring slots and
+//           -> fp32, 6 MMAs of K=16 per K step), tcgen05.commit frees ring slots and
 //           finally signals the epilogue;
 //   warps 2-5 epilogue: tcgen05.ld 32 columns at a time, fused
 //           y = deg*x - Ax; v = mu v + y; raw = x + alpha v; finite check; clamp
@@ -34,8 +34,8 @@ namespace lcb {
 namespace {
 
 constexpr int kBM = 128;                          // rows of A per CTA (UMMA M)
-constexpr int kBK = 64;                           // K per stage (64 bf16 = one 128-byte swizzle row)
-constexpr int kStages = 2;
+constexpr int kBK = 32;                           // K per stage (32 bf16 = one 64-byte swizzle row)
+constexpr int kStages = 4;                        // 4 x 56 KB: three stages in flight while one is consumed
 constexpr int kATileBytes = kBM * kBK * 2;        // 16 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -70,14 +70,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
-__device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t saddr) {
+// K-major operand, 64-byte swizzle: rows of 64 B (kBK bf16), 8-row atoms 512 B apart.
+__device__ __forceinline__ uint64_t umma_desc_k_sw64(uint32_t saddr) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);       // start address
     d |= static_cast<uint64_t>(1u) << 16;                      // LBO (unused for swizzled K-major) = 16 B
-    d |= static_cast<uint64_t>(1024u >> 4) << 32;              // SBO = 1024 B between 8-row groups
+    d |= static_cast<uint64_t>(512u >> 4) << 32;               // SBO = 512 B between 8-row groups
     d |= static_cast<uint64_t>(1u) << 46;                      // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(2u) << 61;                      // SWIZZLE_128B
+    d |= static_cast<uint64_t>(4u) << 61;                      // SWIZZLE_64B
     return d;
 }
 
@@ -183,7 +183,7 @@ template <int N>
 __global__ void __launch_bounds__(192, 1)
     k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP, DenseArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile
+    constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile (multiple of 512)
     constexpr int kStageBytes = kATileBytes + 3 * kPlaneTile;
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], acc_bar;
     __shared__ uint32_t tmem_base_sh;
@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(192, 1)
                 for (int p = 0; p < 3; ++p)
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t da = umma_desc_k_sw128(st + kk * 32);
-                        const uint64_t db = umma_desc_k_sw128(st + kATileBytes + p * kPlaneTile + kk * 32);
+                        const uint64_t da = umma_desc_k_sw64(st + kk * 32);
+                        const uint64_t db = umma_desc_k_sw64(st + kATileBytes + p * kPlaneTile + kk * 32);
                         umma_bf16(tmem, da, db, idesc, (k | p | kk) != 0);
                     }
                 umma_commit(&empty_bar[s]);  // slot free once these MMAs have read it
@@ -379,7 +379,7 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
     const cuuint32_t box[2] = {box_inner, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Failure{4, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r))};
 }

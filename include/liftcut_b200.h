@@ -37,7 +37,7 @@ enum lcb_status {
  * (fp32 state and velocity, same algorithm, checked norm-wise). */
 enum lcb_precision { LCB_FP64 = 0, LCB_FP32 = 1 };
 
-typedef struct lcb_graph lcb_graph; /* device-resident CSR (+ host copy) */
+typedef struct lcb_graph lcb_graph; /* device-resident CSR */
 typedef struct lcb_comm lcb_comm;   /* NCCL communicator over the ranks of one box */
 
 const char* lcb_last_error(void);
@@ -48,7 +48,7 @@ int lcb_device_count(int* count);
  * offsets int64[n+1] / adjacency uint32[offsets[n]] exactly as Graph stores them
  * (sorted, deduplicated, symmetric — graph.cpp:15-50).  The handle keeps a device
  * copy (int32 row pointers / columns, degree vector, degree-descending row order)
- * and a host copy for component splitting. */
+ * (the adjacency is copied back to the host only for a per-component solve). */
 int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacency, int device,
                      lcb_graph** out);
 void lcb_graph_destroy(lcb_graph* g);

@@ -59,8 +59,6 @@ struct DevGraph {
     uint16_t* res_col = nullptr;  // [padded nnz]
     void* dense_A = nullptr;      // bf16 [n][roundup(n,8)] adjacency for the tensor-core path (dense graphs)
     int* res_perm = nullptr;      // [n] new row -> original row (== order)
-    std::vector<int64_t> h_off;
-    std::vector<uint32_t> h_adj;
 };
 
 // ---------------------------------------------------------------------------

@@ -187,8 +187,6 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     g.n = static_cast<int>(n);
     g.nnz = nnz;
     g.m = nnz / 2;
-    g.h_off.assign(off, off + n + 1);
-    g.h_adj.assign(adj, adj + nnz);
     std::vector<int> rp(n + 1), deg(n), ord(n);
     std::vector<double> d64(n);
     std::vector<float> d32(n);
@@ -213,8 +211,6 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     g.deg_sd = std::sqrt(g.deg_var);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return deg[a] > deg[b]; });
-    std::vector<int> colv(static_cast<size_t>(nnz));
-    for (int64_t k = 0; k < nnz; ++k) colv[static_cast<size_t>(k)] = static_cast<int>(adj[k]);
 
     DeviceScope ds(device);
     CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));
@@ -223,7 +219,8 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     CK(cudaMalloc(&g.deg32, sizeof(float) * n));
     CK(cudaMalloc(&g.order, sizeof(int) * n));
     h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
-    if (nnz) h2d(g.col, colv.data(), sizeof(int) * nnz, 0);
+    // uint32 ids < n < 2^31: the same bits as int32, uploaded straight from the caller
+    if (nnz) h2d(g.col, adj, sizeof(int) * nnz, 0);
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
@@ -1338,9 +1335,23 @@ void solve_graph(const DevGraph& g, const lcb_config& cfg, uint64_t seed, const 
     out.search_s += s.search_s;
 }
 
+// host copy of the device CSR, fetched only for per-component solves
+struct HostCSR {
+    std::vector<int> off, adj;
+};
+HostCSR fetch_csr(const DevGraph& g) {
+    HostCSR h;
+    h.off.resize(static_cast<size_t>(g.n) + 1);
+    h.adj.resize(static_cast<size_t>(g.nnz));
+    CK(cudaMemcpy(h.off.data(), g.row_ptr, sizeof(int) * h.off.size(), cudaMemcpyDeviceToHost));
+    if (g.nnz) CK(cudaMemcpy(h.adj.data(), g.col, sizeof(int) * h.adj.size(), cudaMemcpyDeviceToHost));
+    count_d2h(sizeof(int) * (h.off.size() + h.adj.size()));
+    return h;
+}
+
 // connected components, graph.cpp:75-99
-std::vector<std::vector<uint32_t>> components(const DevGraph& g) {
-    const uint32_t n = static_cast<uint32_t>(g.n);
+std::vector<std::vector<uint32_t>> components(const HostCSR& h) {
+    const uint32_t n = static_cast<uint32_t>(h.off.size() - 1);
     std::vector<std::vector<uint32_t>> out;
     std::vector<char> seen(n, 0);
     std::vector<uint32_t> stack;
@@ -1353,8 +1364,8 @@ std::vector<std::vector<uint32_t>> components(const DevGraph& g) {
             const uint32_t v = stack.back();
             stack.pop_back();
             comp.push_back(v);
-            for (int64_t k = g.h_off[v]; k < g.h_off[v + 1]; ++k) {
-                const uint32_t u = g.h_adj[static_cast<size_t>(k)];
+            for (int k = h.off[v]; k < h.off[v + 1]; ++k) {
+                const uint32_t u = static_cast<uint32_t>(h.adj[static_cast<size_t>(k)]);
                 if (!seen[u]) {
                     seen[u] = 1;
                     stack.push_back(u);
@@ -1407,7 +1418,8 @@ void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_
         return;
     }
     // solve_per_component — solver.cpp:314-364
-    const auto comps = components(g);
+    const HostCSR hc = fetch_csr(g);
+    const auto comps = components(hc);
     if (comps.size() == 1 && g.m > 0) {
         solve_graph<T>(g, cfg, seed, o, w, sinks, assignment, out);
         finish();
@@ -1430,8 +1442,8 @@ void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_
         std::vector<uint32_t> adj;
         for (uint32_t i = 0; i < k; ++i) {
             const uint32_t v = comp[i];
-            for (int64_t q = g.h_off[v]; q < g.h_off[v + 1]; ++q) {
-                const uint32_t u = g.h_adj[static_cast<size_t>(q)];
+            for (int q = hc.off[v]; q < hc.off[v + 1]; ++q) {
+                const uint32_t u = static_cast<uint32_t>(hc.adj[static_cast<size_t>(q)]);
                 if (local[u] != static_cast<uint32_t>(g.n)) adj.push_back(local[u]);
             }
             off[i + 1] = static_cast<int64_t>(adj.size());

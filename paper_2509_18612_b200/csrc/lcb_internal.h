@@ -129,6 +129,11 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
                           void* planes, cudaStream_t s, int col_base, float* partial);
 size_t dense_partial_floats();
+// L2-panel path (lcb_narrow.cu): all iterations for one narrow column panel
+int narrow_panel_cols(int elem_bytes);
+template <typename T>
+void run_narrow_panel(const StepArgs<T>& base, const T* X_in, T* X_out, int64_t ld, int c0, int w, int64_t iters,
+                      T* P0, T* P1, T* PV, cudaStream_t s);
 void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
 
 template <typename T>

@@ -614,9 +614,11 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         w.resident_iters += iters;
         return r;
     }
-    // L2-panel member chunking (SURVEY 7 "throughput kernels"): when the iterate is far
-    // larger than L2, run all T iterations for one 128-column slab at a time so the slab's
-    // x-panel (read deg times per iteration by the gathers) stays L2-resident.
+    // K1n, L2-panel member chunking (SURVEY 7 "throughput kernels"): when the iterate is
+    // far larger than L2, run all T iterations on one narrow column panel at a time,
+    // copied into a contiguous [n][P] buffer so the panel that the gathers read deg
+    // times per iteration stays L2-resident (lcb_narrow.cu).  Velocity starts at zero
+    // (ascent.cpp:57) and is not needed afterwards.
     {
         static const int64_t l2 = [] {
             int v = 0;
@@ -625,25 +627,36 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         }();
         static const int chunk_mode = [] {
             const char* e = std::getenv("LCB_CHUNK");
-            return e ? std::atoi(e) : -1;
+            // 0 never (default), 1 always, -1 auto (iterate > 2 x L2 and the panel pair fits).
+            // Off by default: on config 4 (ER 1M, W=512) the panel kernel is latency-bound at
+            // 5.5 ms/iteration vs 4.46 ms for K1 (profiles/round1_narrow.md).
+            return e ? std::atoi(e) : 0;
         }();
-        const int span = step_span<T>(W);
+        const int P = narrow_panel_cols(static_cast<int>(sizeof(T)));
         const int64_t panel = static_cast<int64_t>(g.n) * W * static_cast<int64_t>(sizeof(T));
-        const int64_t slab_panel = static_cast<int64_t>(g.n) * span * static_cast<int64_t>(sizeof(T));
-        const bool want = chunk_mode == 1 || (chunk_mode != 0 && panel > l2 && slab_panel * 3 <= l2);
-        if (want && !ee && !trace_host && W > span) {
+        const int64_t narrow = static_cast<int64_t>(g.n) * P * static_cast<int64_t>(sizeof(T));
+        const bool want = chunk_mode == 1 || (chunk_mode != 0 && panel > 2 * l2 && narrow * 3 <= l2);
+        if (want && !ee && !trace_host && iters > 0 && iters <= 0x7fffffff) {
+            const size_t cells = static_cast<size_t>(g.n) * P;
+            T* P0 = w.Y.ensure(3 * cells);
             CK(cudaEventRecord(w.ev0, w.st));
-            for (int c0 = 0; c0 < W; c0 += span) {
-                StepArgs<T> b = a;
-                b.W = std::min(span, W - c0);
-                b.col_base = c0;
-                b.vel = w.V.p + c0;
-                for (int64_t i = 0; i < iters; ++i) {
-                    b.x_in = w.X[i & 1].p + c0;
-                    b.x_out = w.X[(i + 1) & 1].p + c0;
-                    b.it = static_cast<int>(i);
-                    launch_step<T>(b, false, MODE_STEP, w.st);
+            int64_t launches = 0;
+            double updates = 0.0;
+            // degree order only pays for skewed graphs (warps then hold rows of equal
+            // degree); otherwise it is one more dependent load per row
+            StepArgs<T> na = a;
+            if (static_cast<double>(g.max_degree) <= 4.0 * g.deg_mean + 16.0) na.order = nullptr;
+            for (int c0 = 0; c0 < W; c0 += P) {
+                const int wc = std::min(P, W - c0);
+                int64_t pit = iters;
+                if (seg_iters && err_seg > 0) {  // descending T: the panel's first segment is its longest
+                    const size_t seg = static_cast<size_t>(c0 / (err_seg * l));
+                    if (seg < seg_iters->size()) pit = (*seg_iters)[seg];
                 }
+                run_narrow_panel<T>(na, w.X[0].p, w.X[1].p, w.ld, c0, wc, pit, P0, P0 + cells, P0 + 2 * cells,
+                                    w.st);
+                launches += pit + 2;
+                updates += static_cast<double>(pit) * g.n * wc;
             }
             CK(cudaEventRecord(w.ev1, w.st));
             CK(cudaGetLastError());
@@ -652,19 +665,19 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             r.err = w.h_keys[0];
             r.errs.assign(w.h_keys, w.h_keys + err_slots);
             r.iters = iters;
-            r.final_buf = static_cast<int>(iters & 1);
+            r.final_buf = 1;
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
-            const int chunks = (W + span - 1) / span;
+            const double panels = static_cast<double>((W + P - 1) / P);
             w.step_ms += ms;
-            w.step_launches += iters * chunks;
+            w.step_launches += launches;
             const double bytes = static_cast<double>(iters) *
-                                 (4.0 * sizeof(T) * static_cast<double>(g.n) * W + chunks * (4.0 * g.nnz + 4.0 * (g.n + 1)));
+                                 (4.0 * sizeof(T) * static_cast<double>(g.n) * W + panels * (4.0 * g.nnz + 4.0 * (g.n + 1)));
             w.step_bytes += bytes;
             w.kstats[0] += ms;
-            w.kstats[1] += static_cast<double>(iters * chunks);
+            w.kstats[1] += static_cast<double>(launches);
             w.kstats[2] += bytes;
-            w.node_updates += iters * static_cast<int64_t>(g.n) * W;
+            w.node_updates += static_cast<int64_t>(updates);
             return r;
         }
     }

@@ -375,14 +375,15 @@ def test_batched_search_rounds_match_sequential_and_reference(golden):
 
 
 def test_l2_panel_chunked_driver_bitwise(tmp_path):
-    """The column-chunked T loop (forced with LCB_CHUNK=1) gives the same fp64 bits."""
+    """The L2-panel path (K1n, forced with LCB_CHUNK=1) gives the same fp64 bits, fp32 within
+    tolerance, and the same solver records (early tlim segments inside a panel)."""
     import os
     import subprocess
     import sys
 
     code = (
         "import numpy as np, oracle as O\n"
-        "from paper_2509_18612_b200 import liftcut as lc, LCB_FP64\n"
+        "from paper_2509_18612_b200 import liftcut as lc, LCB_FP64, LCB_FP32\n"
         "cg = O.generate_er(20000, 0.0004, 5)\n"
         "g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)\n"
         "rng = np.random.default_rng(1)\n"
@@ -392,6 +393,19 @@ def test_l2_panel_chunked_driver_bitwise(tmp_path):
         "    s = lc.DenseState(cg.n, l, B); s.values[:] = x\n"
         "    lc.ascend(g, s, lc.AscentParams(0.05, 12, 0.9, False), precision=LCB_FP64)\n"
         "    assert np.array_equal(s.values, want), (l, B)\n"
+        "    s32 = lc.DenseState(cg.n, l, B); s32.values[:] = x\n"
+        "    lc.ascend(g, s32, lc.AscentParams(0.05, 12, 0.9, False), precision=LCB_FP32)\n"
+        "    assert np.linalg.norm(s32.values - want) <= 1e-5 * np.linalg.norm(want), (l, B)\n"
+        "cg2 = O.generate_er(300, 0.03, 3)\n"
+        "g2 = lc.Graph.from_csr(cg2.n, cg2.off, cg2.adj)\n"
+        "cfg = lc.SolverConfig(batch_size=64, num_batches=2, ascent=lc.AscentParams(0.05, 60),\n"
+        "                      search=lc.SearchConfig(20, 80, -3.0, -1.0, 6, 3))\n"
+        "w = O.solve(cg2, O.default_config(batch_size=64, num_batches=2, iterations=60, has_search=1, t_lower=20,\n"
+        "            t_upper=80, e_lower=-3.0, e_upper=-1.0, population_size=6, rounds=3), 11)\n"
+        "for bs in (False, True):\n"
+        "    b = lc.pquco(g2, cfg, 11, opts=lc.RunOptions(precision=LCB_FP64, batched_search=bs))\n"
+        "    assert b.best.cut_value == w.cut_value and b.best.assignment.tolist() == w.assignment.tolist(), bs\n"
+        "    assert b.kernel_stats['k_step'][1] > 0 and b.kernel_stats['k_resident'][1] == 0\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,

@@ -3,13 +3,14 @@ pLUCO batch (l=2, W=2B) with early exit off; prints CUDA-event ms per step launc
 and per iteration, and node-updates/s of the T loop.
 
     python tools/kbench.py [--B 1024] [--T 200] [--precision fp32] [--n 10000]
+    python tools/kbench.py --graph er --n 1000000 --B 512 --T 20 --quco-only   # config-4 graph
 """
 import argparse
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import ba_graph  # noqa: E402
+from bench import ba_graph, er_sparse  # noqa: E402
 from paper_2509_18612_b200 import LCB_FP32, LCB_FP64  # noqa: E402
 from paper_2509_18612_b200 import liftcut as lc  # noqa: E402
 
@@ -19,10 +20,12 @@ ap.add_argument("--T", type=int, default=200)
 ap.add_argument("--n", type=int, default=10000)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--tag", default="")
+ap.add_argument("--graph", default="ba", choices=["ba", "er"])
+ap.add_argument("--quco-only", action="store_true")
 a = ap.parse_args()
-g = ba_graph(a.n, 4, 0)
+g = ba_graph(a.n, 4, 0) if a.graph == "ba" else er_sparse(a.n, 10.0, 0)
 prec = LCB_FP32 if a.precision == "fp32" else LCB_FP64
-for algo, l in ((lc.Algorithm.pQUCO, 1), (lc.Algorithm.pLUCO, 2)):
+for algo, l in ((lc.Algorithm.pQUCO, 1), (lc.Algorithm.pLUCO, 2))[:1 if a.quco_only else 2]:
     cfg = lc.SolverConfig(algorithm=algo, batch_size=a.B, lift_dim=2,
                           ascent=lc.AscentParams(0.05, a.T, 0.9, False), num_batches=1)
     fn = lc.pquco if l == 1 else lc.pluco

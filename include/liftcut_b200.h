@@ -78,6 +78,17 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
                         int32_t lifted, int64_t* cuts, int64_t* best_member, int64_t* best_cut,
                         uint8_t* best_z);
 
+/* Exhaustive MaxCut (brute_force_maxcut, oracle.hpp:18-22 / oracle.cpp:50-99) on the
+ * device: Gray-code scan of the 2^(n-1) assignments with node 0 fixed.
+ * - count_optimal counts z and its complement separately.
+ * - witness [n] is the optimal assignment with the smallest integer encoding of
+ *   min(z, ~z).
+ * - max_nodes = 0 keeps the reference guard (n <= 26, LCB_VALIDATION above it).
+ * - Larger values, up to 40, lift the guard.
+ * - count_optimal and witness are optional. */
+int lcb_brute_force_maxcut(const lcb_graph* g, int32_t max_nodes, int64_t* optimum, int64_t* count_optimal,
+                           uint8_t* witness);
+
 /* ---- init (init.hpp:37-52, init.cpp:20-101) ---------------------------------
  * Stream keys are RngStream::key() values (rng.hpp:27-79).  DUI / IDI / the lifted
  * mean are integer-exact; gaussian_batch draws its normals on the device (CUDA

@@ -389,6 +389,16 @@ class RefGraph:
             self.h = None
 
 
+def ref_brute_force_maxcut(rg: RefGraph):
+    """The reference ``brute_force_maxcut`` (oracle.cpp:50-99) -> (optimum, witness, count)."""
+    w = np.zeros(rg.n, dtype=np.uint8)
+    cnt = C.c_int64(0)
+    best = ref.ref_brute_force(rg.h, _ptr(w), C.byref(cnt))
+    if best < 0:
+        raise OracleError(1, ref.ref_last_error().decode())
+    return int(best), w, int(cnt.value)
+
+
 def ref_ascend(rg: RefGraph, values, l, B, alpha=0.05, T=500, mu=0.9, early_exit=True,
                workers=1, trace=False):
     v = np.array(values, dtype=np.float64, copy=True).reshape(-1)

@@ -77,6 +77,7 @@ SIGNATURES = {
     "lcb_ascend": (C.c_int, [P, P, i64, i32, i64, f64, i64, f64, i32, i32, P, P, P]),
     "lcb_cut_values": (C.c_int, [P, P, i64, P]),
     "lcb_round_cut_batch": (C.c_int, [P, P, i32, i64, i32, P, P, P, P]),
+    "lcb_brute_force_maxcut": (C.c_int, [P, i32, P, P, P]),
     "lcb_dui_init": (C.c_int, [P, u64, P]),
     "lcb_idi_init": (C.c_int, [P, f64, u64, P]),
     "lcb_lifted_init_mean": (C.c_int, [P, i32, f64, i32, u64, P]),

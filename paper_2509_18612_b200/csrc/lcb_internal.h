@@ -134,6 +134,11 @@ int narrow_panel_cols(int elem_bytes);
 template <typename T>
 void run_narrow_panel(const StepArgs<T>& base, const T* X_in, T* X_out, int64_t ld, int c0, int w, int64_t iters,
                       T* P0, T* P1, T* PV, cudaStream_t s);
+// exhaustive MaxCut (lcb_oracle.cu)
+int brute_force_max_layers();
+size_t brute_force_scratch_bytes();
+const void* launch_brute_force(const uint64_t* masks, const uint64_t* upper, const int* deg, int n, int layers,
+                               void* scratch, cudaStream_t s);
 void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
 
 template <typename T>

@@ -375,6 +375,7 @@ struct Work {
     DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes
     DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
     DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
+    DBuf<uint64_t> bf;           // exhaustive scan: masks, upper masks, degrees, block records
     unsigned long long* h_keys = nullptr;  // pinned
     uint32_t* h_flags = nullptr;
     size_t h_flags_cap = 0;
@@ -1669,6 +1670,61 @@ int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t*
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
         for (int64_t i = 0; i < count; ++i) cuts[i] = static_cast<int64_t>(h[static_cast<size_t>(i)]);
+    });
+}
+
+int lcb_brute_force_maxcut(const lcb_graph* g, int32_t max_nodes, int64_t* optimum, int64_t* count_optimal,
+                           uint8_t* witness) {
+    return guard([&] {
+        if (!g || !optimum) fail(LCB_VALIDATION, "null argument");
+        const DevGraph& G = g->g;
+        const int guard_n = max_nodes > 0 ? max_nodes : 26;  // oracle.cpp:53-55
+        if (guard_n > 40) fail(LCB_VALIDATION, "brute_force_maxcut: max_nodes above 40 is out of reach");
+        if (G.n > guard_n)
+            fail(LCB_VALIDATION, "brute_force_maxcut: n = " + std::to_string(G.n) +
+                                     " exceeds the exhaustive-scan guard (" + std::to_string(guard_n) + ")");
+        const int n = G.n;
+        const HostCSR hc = fetch_csr(G);
+        // neighbour masks, one layer per multiplicity level (a raw CSR may repeat entries)
+        const int max_layers = brute_force_max_layers();
+        std::vector<uint64_t> masks(static_cast<size_t>(max_layers) * n, 0), upper(masks.size(), 0);
+        std::vector<int> deg(static_cast<size_t>(n));
+        int layers = 1;
+        for (int u = 0; u < n; ++u) {
+            deg[static_cast<size_t>(u)] = hc.off[static_cast<size_t>(u) + 1] - hc.off[static_cast<size_t>(u)];
+            for (int k = hc.off[static_cast<size_t>(u)]; k < hc.off[static_cast<size_t>(u) + 1]; ++k) {
+                const int v = hc.adj[static_cast<size_t>(k)];
+                int layer = 0;
+                while (layer < max_layers && (masks[static_cast<size_t>(layer) * n + u] >> v & 1ull)) ++layer;
+                if (layer == max_layers) fail(LCB_VALIDATION, "brute_force_maxcut: edge multiplicity above 4");
+                masks[static_cast<size_t>(layer) * n + u] |= 1ull << v;
+                if (v > u) upper[static_cast<size_t>(layer) * n + u] |= 1ull << v;
+                layers = std::max(layers, layer + 1);
+            }
+        }
+        DeviceScope ds(G.device);
+        PooledWork<double> pw(G.device);
+        Work<double>& w = *pw;
+        const size_t mwords = static_cast<size_t>(layers) * n;
+        const size_t dwords = (static_cast<size_t>(n) + 1) / 2;
+        const size_t swords = (brute_force_scratch_bytes() + 7) / 8;
+        uint64_t* d = w.bf.ensure(2 * mwords + dwords + swords + 1);
+        uint64_t* dm = d;
+        uint64_t* du = d + mwords;
+        int* dd = reinterpret_cast<int*>(d + 2 * mwords);
+        void* scratch = d + 2 * mwords + dwords + 1;
+        h2d(dm, masks.data(), sizeof(uint64_t) * mwords, w.st);
+        h2d(du, upper.data(), sizeof(uint64_t) * mwords, w.st);
+        h2d(dd, deg.data(), sizeof(int) * static_cast<size_t>(n), w.st);
+        const void* fin = launch_brute_force(dm, du, dd, n, layers, scratch, w.st);
+        unsigned long long rec[3];
+        d2h(rec, fin, sizeof(rec), w.st);
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+        *optimum = static_cast<int64_t>(static_cast<long long>(rec[0]));
+        if (count_optimal) *count_optimal = static_cast<int64_t>(rec[1]);
+        if (witness)
+            for (int v = 0; v < n; ++v) witness[v] = static_cast<uint8_t>((rec[2] >> v) & 1ull);
     });
 }
 

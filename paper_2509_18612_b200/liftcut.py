@@ -516,6 +516,26 @@ def round_cut_batch(g: Graph, state: DenseState, lifted: bool):
     return cuts, bm.value, bc.value, z
 
 
+@dataclass
+class OracleResult:
+    """oracle.hpp:12-16."""
+    optimum: int
+    witness: np.ndarray
+    count_optimal: int  # z and its complement counted separately
+
+
+def brute_force_maxcut(g: Graph, workers: int = 1, max_nodes: int = 0) -> OracleResult:
+    """Exhaustive MaxCut (oracle.hpp:18-22) as one device Gray-code scan.  ``workers``
+    is accepted for signature parity; the result never depended on it.  ``max_nodes``
+    lifts the reference's n <= 26 guard (up to 40)."""
+    del workers
+    n = g.node_count()
+    z = np.zeros(n, dtype=np.uint8)
+    opt, cnt = C.c_int64(), C.c_int64()
+    _check(_abi.lib().lcb_brute_force_maxcut(g.handle(), int(max_nodes), C.byref(opt), C.byref(cnt), _ptr(z)))
+    return OracleResult(opt.value, z, cnt.value)
+
+
 def project_box(values):
     np.clip(values, -1.0, 1.0, out=values)
 

@@ -165,3 +165,19 @@ def test_random_against_reference(seed):
         r1, r2 = O.solve(g, cfg, seed), O.ref_solve(rg, cfg, seed)
         assert (r1.cut_value, r1.batch_index, r1.member_index) == (r2.cut_value, r2.batch_index, r2.member_index)
         assert np.array_equal(r1.assignment, r2.assignment) and r1.batch_trace == r2.batch_trace
+
+
+@needs_ref
+def test_brute_force_against_reference():  # oracle.cpp:50-99, test_oracle.cpp:36-120
+    rng = np.random.default_rng(7)
+    for n in (1, 2, 3, 7, 11, 16):
+        for p in (0.2, 0.5, 0.9):
+            eu, ev = np.triu_indices(n, 1)
+            keep = rng.random(len(eu)) < p
+            cg = O.csr_from_edges(n, eu[keep], ev[keep])
+            best, w, cnt = O.brute_force_maxcut(cg)
+            rb, rw, rc = O.ref_brute_force_maxcut(O.RefGraph.from_edges(n, eu[keep], ev[keep]))
+            assert (best, w.tolist(), cnt) == (rb, rw.tolist(), rc), (n, p)
+    with pytest.raises(O.OracleError):
+        O.ref_brute_force_maxcut(O.RefGraph.from_edges(27, [0], [1]))
+

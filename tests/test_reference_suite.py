@@ -1,6 +1,6 @@
 """The reference's OWN unit tests (proj/tests/test_*.cpp, unchanged), compiled against
-the B200 drop-in (paper_2509_18612_b200/dropin: ascent.cpp / init.cpp / solver.cpp
-replaced by libliftcut_b200.so-backed files behind the unchanged reference headers)
+the B200 drop-in (paper_2509_18612_b200/dropin: ascent.cpp / init.cpp / oracle.cpp /
+solver.cpp replaced by libliftcut_b200.so-backed files behind the unchanged reference headers)
 with the doctest-compatible harness in tests/refsuite/doctest.h.
 
 The binary is built where /root/reference exists (`make -C paper_2509_18612_b200/dropin
@@ -24,13 +24,13 @@ def run_suites(suites, env=None, exclude=None):
 
 @needs_bin
 def test_reference_suites_on_kept_host_code():
-    code, out = run_suites(["rng", "parallel", "graph", "objectives", "evo", "oracle"])
+    code, out = run_suites(["rng", "parallel", "graph", "objectives", "evo"])
     assert code == 0, out[-3000:]
 
 
 @needs_bin
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["ascent", "init", "solver"])
+@pytest.mark.parametrize("suite", ["ascent", "init", "oracle", "solver"])
 def test_reference_suite_against_b200_dropin(suite):
     code, out = run_suites([suite])
     assert code == 0 and "0 failed" in out, out[-4000:]

@@ -57,6 +57,7 @@ struct DevGraph {
     int* res_heavy = nullptr;     // [heavy][2] absolute word offset, degree
     int res_nheavy = 0;
     uint16_t* res_col = nullptr;  // [padded nnz]
+    uint16_t* res_col_fast = nullptr;  // fp32 copy, light rows in bank-balanced order (or null)
     void* dense_A = nullptr;      // bf16 [n][roundup(n,8)] adjacency for the tensor-core path (dense graphs)
     int* res_perm = nullptr;      // [n] new row -> original row (== order)
 };

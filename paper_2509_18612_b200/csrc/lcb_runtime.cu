@@ -166,9 +166,10 @@ void free_graph(DevGraph& g) {
     cudaFree(g.dense_A);
     g.dense_A = nullptr;
     cudaFree(g.res_col);
+    cudaFree(g.res_col_fast);
     g.res_info = nullptr;
     g.row_ptr = g.col = g.order = g.res_chunk = nullptr;
-    g.res_col = nullptr;
+    g.res_col = g.res_col_fast = nullptr;
     g.res_perm = nullptr;
     g.deg64 = nullptr;
     g.deg32 = nullptr;
@@ -280,6 +281,63 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                 int64_t o = rrp[r];
                 for (int64_t k = off[v]; k < off[v + 1]; ++k) rcol[static_cast<size_t>(o++)] = static_cast<uint16_t>(inv[adj[k]]);
             }
+            // fp32 copy with a bank-balanced neighbour order: the 32 light rows of a warp
+            // gather their p-th neighbours in the same LDS instruction, and an 8-byte slot s
+            // sits in bank pair s mod 16, so the wavefront count of that instruction is the
+            // largest number of distinct slots in one bank pair.  A greedy pass picks each
+            // row's p-th neighbour from its remaining ones to keep that maximum low
+            // (BA 10k: 4.10 -> 3.01 on average).  fp32 only: the fp64 path keeps CSR order
+            // for bit-exact sums (graph.cpp:118).
+            static const bool bank_order = [] {
+                const char* e = std::getenv("LCB_BANK_ORDER");
+                return !e || std::atoi(e) != 0;
+            }();
+            std::vector<uint16_t> fast;
+            if (bank_order) {
+                fast = rcol;
+                std::vector<std::vector<uint16_t>> rem(32);
+                std::vector<int> idx;
+                idx.reserve(32);
+                std::vector<int> stamp(static_cast<size_t>(n) + 1, -1);  // slot already gathered in this step
+                int step_id = 0;
+                for (uint32_t b0 = static_cast<uint32_t>(H); b0 < n; b0 += 32) {
+                    const uint32_t b1 = std::min<uint32_t>(b0 + 32, n);
+                    const int rows = static_cast<int>(b1 - b0);
+                    int L = 0;
+                    for (int i = 0; i < rows; ++i) {
+                        const uint32_t r = b0 + static_cast<uint32_t>(i);
+                        const int d = deg[ord[r]];
+                        rem[i].assign(rcol.begin() + rrp[r], rcol.begin() + rrp[r] + d);
+                        L = std::max(L, d);
+                    }
+                    for (int p = 0; p < L; ++p, ++step_id) {
+                        int cnt[16] = {0};
+                        idx.clear();
+                        for (int i = 0; i < rows; ++i)
+                            if (!rem[i].empty()) idx.push_back(i);
+                        std::stable_sort(idx.begin(), idx.end(),
+                                         [&](int x, int y) { return rem[x].size() < rem[y].size(); });
+                        for (int i : idx) {
+                            int bj = 0, bc = 1 << 30;
+                            for (int j = 0; j < static_cast<int>(rem[i].size()); ++j) {
+                                const uint16_t u = rem[i][j];
+                                const int c = stamp[u] == step_id ? -1 : cnt[u & 15];
+                                if (c < bc) {
+                                    bc = c;
+                                    bj = j;
+                                }
+                            }
+                            const uint16_t u = rem[i][bj];
+                            rem[i].erase(rem[i].begin() + bj);
+                            fast[static_cast<size_t>(rrp[b0 + i] + p)] = u;
+                            if (bc >= 0) {
+                                stamp[u] = step_id;
+                                ++cnt[u & 15];
+                            }
+                        }
+                    }
+                }
+            }
             CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * info.size()));
             CK(cudaMalloc(&g.res_chunk, sizeof(int) * chunks));
             CK(cudaMalloc(&g.res_heavy, sizeof(int) * hinfo.size()));
@@ -289,6 +347,10 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             h2d(g.res_heavy, hinfo.data(), sizeof(int) * hinfo.size(), 0);
             g.res_nheavy = H;
             h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
+            if (!fast.empty()) {
+                CK(cudaMalloc(&g.res_col_fast, sizeof(uint16_t) * fast.size()));
+                h2d(g.res_col_fast, fast.data(), sizeof(uint16_t) * fast.size(), 0);
+            }
         }
     }
 }
@@ -575,7 +637,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         ra.chunk_base = g.res_chunk;
         ra.heavy_info = g.res_heavy;
         ra.heavy = g.res_nheavy;
-        ra.col = g.res_col;
+        ra.col = (sizeof(T) == 4 && g.res_col_fast) ? g.res_col_fast : g.res_col;
         ra.perm = g.res_perm;
         ra.X = w.X[0].p;
         ra.ld = w.ld;

@@ -529,8 +529,7 @@ struct PooledWork {
 
 // Kernel choice measured on B200 (profiles/round1_kernel_ab.md): the member-resident
 // kernel wins when the on-chip slab covers the graph and the batch is wide enough to
-// fill whole waves (W >= 2048 columns at K=2, any W for fp64 / small graphs); the
-// HBM-streaming kernel wins for the narrow fp32 batch (W = 1024: 51 vs 62 us/iteration).
+// fill several waves (W >= 1024 columns at K=2, any W for fp64 / small graphs).
 bool resident_preferred(const DevGraph& g, int W, size_t elem) {
     static const int mode = [] {
         const char* e = std::getenv("LCB_RESIDENT");
@@ -540,7 +539,7 @@ bool resident_preferred(const DevGraph& g, int W, size_t elem) {
     if (mode == 1) return true;
     if (elem == 8) return true;
     if (g.n <= 2048) return true;  // whole batch on chip, launch-latency bound otherwise
-    return W >= 2048;
+    return W >= 1024;  // with the bank-balanced order: W=1024 48.1 vs 51.2 us/iteration (K1)
 }
 
 struct IterResult {

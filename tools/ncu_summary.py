@@ -44,7 +44,7 @@ def main(paths):
     summary = {}
     print("| kernel | metric | value |\n|---|---|---|")
     for p in paths:
-        for d in raw(p):
+        for idx, d in enumerate(raw(p)):
             name = d.get("Kernel Name", ("?", ""))[0].split("(")[0].replace("void ", "")
             e = {}
             for k in KEYS:
@@ -61,7 +61,7 @@ def main(paths):
             wb = e.get("dram__bytes_write.sum", (0, ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             traffic = (rb[0] or 0) * scale.get(rb[1], 1) + (wb[0] or 0) * scale.get(wb[1], 1)
-            summary[os.path.basename(p) + ":" + name] = {
+            summary[f"{os.path.basename(p)}:{idx}:{name}"] = {
                 "dram_bytes_per_launch": traffic,
                 "duration": e.get("gpu__time_duration.sum"),
                 "stalls_top": top,

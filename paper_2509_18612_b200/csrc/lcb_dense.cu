@@ -8,24 +8,33 @@
 // fp32-faithful A·X (executed flops = 3x algorithmic).
 //
 // One CTA per 128-row tile of A (M=128), all N = W (<= 256) columns:
-//   warp 0  TMA producer: A tile [128 x 32] + 3 plane tiles [N x 32] per K step,
-//           64-byte swizzle, 4-stage ring, mbarrier complete_tx;
+//   warp 0  TMA producer: A tile [128 x 32] + plane tiles [N x 32] per K step,
+//           64-byte swizzle, L2 evict-first for A / evict-last for the planes;
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16 x bf16
-//           -> fp32, 6 MMAs of K=16 per K step), tcgen05.commit frees ring slots and
-//           finally signals the epilogue;
-//   warps 2-5 epilogue: tcgen05.ld 32 columns at a time, fused
-//           y = deg*x - Ax; v = mu v + y; raw = x + alpha v; finite check; clamp
-//           (ascent.cpp:66-77), writes x' / v' (fp32, member-major [W][n]) and the
-//           three bf16 planes of x' for the next iteration (planes double-buffered:
-//           every CTA reads all of them).
+//           -> fp32, 2 MMAs of K=16 per plane and K step), tcgen05.commit frees ring
+//           slots and finally signals the epilogue;
+//   warps 2-9 epilogue (two warps per TMEM lane quarter, half the columns each):
+//           tcgen05.ld 32 columns at a time, fused y = deg*x - Ax; v = mu v + y;
+//           raw = x + alpha v; finite check; clamp (ascent.cpp:66-77), writes x' / v'
+//           (fp32, member-major [W][n]) and the three bf16 planes of x' for the next
+//           iteration (planes double-buffered: every CTA reads all of them).
+// Both operands are stored blocked (one contiguous 8 / 16 KB run per TMA box).
+//
+// Zero-plane skipping: once x' sits on the box corners (x = +-1 exactly, after a few
+// iterations on config 3) its mid / lo planes are exactly zero.  The epilogue records,
+// per 32-node K step, whether any mid / lo entry is nonzero; the next launch loads and
+// multiplies only the hi plane for the other K steps (adding A*0 changes nothing), and
+// when at least half the K steps skip it switches the ring to 8 narrower slots.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "lcb_internal.h"
 
@@ -35,8 +44,15 @@ namespace {
 
 constexpr int kBM = 128;                          // rows of A per CTA (UMMA M)
 constexpr int kBK = 32;                           // K per stage (32 bf16 = one 64-byte swizzle row)
-constexpr int kStages = 4;                        // 4 x 56 KB: three stages in flight while one is consumed
-constexpr int kATileBytes = kBM * kBK * 2;        // 16 KB
+constexpr int kStages = 4;                        // full mode: 4 x 56 KB slots (A + 3 planes)
+constexpr int kSkipStages = 8;                    // skip mode: 8 x 24 KB slots (A + hi) + 1 low slot (mid + lo)
+constexpr int kATileBytes = kBM * kBK * 2;        // 8 KB
+constexpr int kMaxFlagWords = 64;
+#ifndef LCB_DENSE_EPI_WARPS
+#define LCB_DENSE_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = LCB_DENSE_EPI_WARPS;   // epilogue warps: 4 (one per TMEM lane quarter) or 8
+constexpr int kThreadsDense = 64 + 32 * kEpiWarps;                 // K-step flags held in SMEM (n <= 65536)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,11 +76,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// long waits (the epilogue waits for the whole main loop): back off between probes so the
+// spinning warps leave the issue slots to the producer / MMA threads
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(256);
+    }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
             "r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -130,10 +172,11 @@ struct DenseArgs {
     const float* deg;        // [n]
     float* X;                // [W][n] member-major fp32 iterate (in place)
     float* V;                // [W][n] velocity (in place)
-    __nv_bfloat16* planes_out;  // [3][W][ldp] planes of x' for the next iteration
+    __nv_bfloat16* planes_out;  // blocked planes of x' for the next iteration (plane_index)
     int n;
     int ldx;                 // row pitch of X / V (elements)
-    int ldp;                 // row pitch of the planes (elements, multiple of 8)
+    int nks;                 // 32-node K steps
+    int nb;                  // member rows per plane block (UMMA N: 64 / 128 / 256)
     int W;                   // live columns (<= 256, multiple of 16)
     int l;
     int col_base;            // first batch column of this launch (column chunks of <= 256)
@@ -147,10 +190,23 @@ struct DenseArgs {
     int tile_base;           // first M-tile of this launch
     int k_split;             // K pieces per tile (1: whole K, fused epilogue)
     float* partial;          // k_split > 1: fp32 partial sums [block][N][128]
+    const uint32_t* kflags_in;  // [K steps] 0: the mid/lo planes of this 32-node K step are all zero
+    uint32_t* kflags_out;       // the same for the planes written by this launch
 };
 
+// Blocked B operand: plane p, K step ks = node / 32 -> one contiguous [nb][32] bf16 block
+// (nb x 64 B), the exact box one TMA load fetches; likewise A is stored as contiguous
+// [128][32] blocks per (M tile, K step), so both operands stream as whole 8-16 KB runs.
+__host__ __device__ __forceinline__ int64_t plane_index(int p, int row, int c, int nks, int nb) {
+    return ((static_cast<int64_t>(p) * nks + (row >> 5)) * nb + c) * 32 + (row & 31);
+}
+__host__ __device__ __forceinline__ int64_t adj_index(int v, int u, int nks) {
+    return ((static_cast<int64_t>(v >> 7) * nks + (u >> 5)) * 128 + (v & 127)) * 32 + (u & 31);
+}
+
 // Fused heavy-ball step for one (row, column) given Ax (ascent.cpp:66-77) + plane split.
-__device__ __forceinline__ void finish_element(const DenseArgs& a, int row, int c, float ax, float dg) {
+// Returns whether the mid / lo planes of x' are nonzero (x' = +-1 exactly splits to hi only).
+__device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int c, float ax, float dg) {
     const int m = (a.col_base + c) / a.l;
     bool act = true;
     float alpha = a.alpha_uniform;
@@ -172,21 +228,33 @@ __device__ __forceinline__ void finish_element(const DenseArgs& a, int row, int 
     }
     __nv_bfloat16 h, mi, lo;
     split3(x, h, mi, lo);
-    const int64_t po = static_cast<int64_t>(c) * a.ldp + row;
-    const int64_t ps = static_cast<int64_t>(a.W) * a.ldp;
+    const int64_t po = plane_index(0, row, c, a.nks, a.nb);
+    const int64_t ps = static_cast<int64_t>(a.nks) * a.nb * 32;
     a.planes_out[po] = h;
     a.planes_out[ps + po] = mi;
     a.planes_out[2 * ps + po] = lo;
+    return ((__bfloat16_as_ushort(mi) | __bfloat16_as_ushort(lo)) & 0x7fffu) != 0;
 }
 
+// Two smem carve-ups of the same ring, chosen per launch from the K-step flags of the
+// previous iteration (all CTAs count them, so all agree):
+//   full mode  kStages slots of A + hi + mid + lo;
+//   skip mode  (>= half of the K steps have all-zero mid / lo planes, i.e. the iterate
+//              sits on the box corners): kSkipStages slots of A + hi, so twice as many
+//              K steps are in flight, and one extra slot for the mid / lo planes of the
+//              few K steps that still need them.
 template <int N>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreadsDense, 1)
     k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP, DenseArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile (multiple of 512)
-    constexpr int kStageBytes = kATileBytes + 3 * kPlaneTile;
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], acc_bar;
+    constexpr int kFullSlot = kATileBytes + 3 * kPlaneTile;
+    constexpr int kSkipSlot = kATileBytes + kPlaneTile;
+    __shared__ __align__(8) uint64_t full_bar[kSkipStages], empty_bar[kSkipStages], low_empty, acc_bar;
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int zero_steps;
+    __shared__ uint32_t qflag[4];                  // per TMEM lane quarter: nonzero mid / lo planes
+    __shared__ uint32_t need_low[kMaxFlagWords];  // bit ks: K step ks needs its mid / lo planes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -199,11 +267,14 @@ __global__ void __launch_bounds__(192, 1)
     // 1024-byte aligned ring
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
 
+    if (threadIdx.x == 0) zero_steps = 0;
+    if (threadIdx.x < 4) qflag[threadIdx.x] = 0u;
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kSkipStages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
+        mbar_init(&low_empty, 1);
         mbar_init(&acc_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -214,23 +285,58 @@ __global__ void __launch_bounds__(192, 1)
                      "n"(N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    __syncthreads();
+    // the flags go to SMEM once: the single producer / MMA threads must not pay a global
+    // load latency per K step
+    const bool flags = a.kflags_in && nk_all <= 32 * kMaxFlagWords;
+    if (flags) {
+        int z = 0;
+        for (int w0 = warp * 32; w0 < nk_all; w0 += 32 * (blockDim.x >> 5)) {
+            const int i = w0 + lane;
+            const bool nz = i >= nk_all || a.kflags_in[i] != 0;
+            const uint32_t b = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) need_low[w0 >> 5] = b;
+            z += 32 - __popc(b);
+        }
+        if (lane == 0 && z) atomicAdd(&zero_steps, z);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    const bool skipmode = flags && 2 * zero_steps >= nk_all;
+    const int S = skipmode ? kSkipStages : kStages;
+    const int slot_bytes = skipmode ? kSkipSlot : kFullSlot;
+    uint8_t* low = ring + kSkipStages * kSkipSlot;  // skip mode only: mid, lo tiles
 
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
+            // A streams once per iteration (evict first); the planes are re-read by every CTA
+            uint64_t pol_a, pol_p;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
+            int low_uses = 0;
             for (int k = 0; k < nk; ++k) {
-                const int s = k % kStages;
-                if (k >= kStages) mbar_wait(&empty_bar[s], ((k / kStages) - 1) & 1);
-                uint8_t* st = ring + s * kStageBytes;
-                mbar_expect_tx(&full_bar[s], kStageBytes);
-                tma_load_2d(st, &tmA, &full_bar[s], (kb + k) * kBK, m0);
-#pragma unroll
-                for (int p = 0; p < 3; ++p)
-                    tma_load_2d(st + kATileBytes + p * kPlaneTile, &tmP, &full_bar[s], (kb + k) * kBK, p * a.W);
+                const int s = k % S;
+                const int ks = kb + k;
+                if (k >= S) mbar_wait(&empty_bar[s], ((k / S) - 1) & 1);
+                uint8_t* st = ring + s * slot_bytes;
+                // all-zero mid / lo planes (every x of these 32 nodes is +-1): skip them
+                const int np = (flags && !((need_low[ks >> 5] >> (ks & 31)) & 1u)) ? 1 : 3;
+                mbar_expect_tx(&full_bar[s], kATileBytes + np * kPlaneTile);
+                tma_load_2d_hint(st, &tmA, &full_bar[s], 0, (tile * a.nks + ks) * kBM, pol_a);
+                tma_load_2d_hint(st + kATileBytes, &tmP, &full_bar[s], 0, ks * N, pol_p);
+                if (np == 3) {
+                    uint8_t* lp = st + kATileBytes + kPlaneTile;
+                    if (skipmode) {
+                        if (low_uses > 0) mbar_wait(&low_empty, (low_uses - 1) & 1);
+                        ++low_uses;
+                        lp = low;
+                    }
+                    tma_load_2d_hint(lp, &tmP, &full_bar[s], 0, (a.nks + ks) * N, pol_p);
+                    tma_load_2d_hint(lp + kPlaneTile, &tmP, &full_bar[s], 0, (2 * a.nks + ks) * N, pol_p);
+                }
             }
         }
     } else if (warp == 1) {
@@ -238,32 +344,41 @@ __global__ void __launch_bounds__(192, 1)
         constexpr uint32_t idesc = idesc_bf16(kBM, N);
         if (lane == 0) {
             for (int k = 0; k < nk; ++k) {
-                const int s = k % kStages;
-                mbar_wait(&full_bar[s], (k / kStages) & 1);
+                const int s = k % S;
+                mbar_wait(&full_bar[s], (k / S) & 1);
                 tc_fence_after();
-                const uint32_t st = smem_u32(ring + s * kStageBytes);
-#pragma unroll
-                for (int p = 0; p < 3; ++p)
+                const uint32_t st = smem_u32(ring + s * slot_bytes);
+                const int ks = kb + k;
+                const int np = (flags && !((need_low[ks >> 5] >> (ks & 31)) & 1u)) ? 1 : 3;  // as the producer
+                const uint32_t lp = (skipmode ? smem_u32(low) : st + kATileBytes + kPlaneTile) - kPlaneTile;
+                for (int p = 0; p < np; ++p)
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint64_t da = umma_desc_k_sw64(st + kk * 32);
-                        const uint64_t db = umma_desc_k_sw64(st + kATileBytes + p * kPlaneTile + kk * 32);
+                        const uint32_t pb = p == 0 ? st + kATileBytes : lp + p * kPlaneTile;
+                        const uint64_t db = umma_desc_k_sw64(pb + kk * 32);
                         umma_bf16(tmem, da, db, idesc, (k | p | kk) != 0);
                     }
                 umma_commit(&empty_bar[s]);  // slot free once these MMAs have read it
+                if (skipmode && np == 3) umma_commit(&low_empty);
             }
             umma_commit(&acc_bar);           // accumulator complete
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue (warps 2..5): TMEM lane quarter = warp % 4
+        // ---------------- epilogue (warps 2..): a warp may only touch TMEM lane quarter
+        // warp % 4; with 8 epilogue warps two warps share a quarter and split the columns
         const int q = warp & 3;
+        constexpr int parts = kEpiWarps / 4;
+        const int part = (warp - 2) / 4;
+        const int cbeg = part * (N / parts), cend = cbeg + N / parts;
         const int row = m0 + q * 32 + lane;
-        mbar_wait(&acc_bar, 0);
+        mbar_wait_sleep(&acc_bar, 0);
         tc_fence_after();
         const bool live = row < a.n;
         const float dg = live ? __ldg(a.deg + row) : 0.f;
-        for (int c0 = 0; c0 < N; c0 += 32) {
+        bool low_nz = false;  // any nonzero mid / lo plane entry in this warp's 32 nodes
+        for (int c0 = cbeg; c0 < cend; c0 += 32) {
             uint32_t r[32];
             tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
             if (a.k_split > 1) {  // split-K piece: fp32 partial sums, coalesced along rows
@@ -276,7 +391,18 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int c = c0 + j;
-                if (c < a.W) finish_element(a, row, c, __uint_as_float(r[j]), dg);
+                if (c < a.W) low_nz |= finish_element(a, row, c, __uint_as_float(r[j]), dg);
+            }
+        }
+        // one lane quarter = one 32-node K step of the next iteration's B operand; split-K
+        // tail tiles: piece 0 clears the flag, k_dense_reduce ORs it in after the pieces
+        if (a.kflags_out) {
+            if (a.k_split == 1) {
+                if (__any_sync(0xffffffffu, low_nz) && lane == 0) atomicOr(&qflag[q], 1u);
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                if (part == 0 && lane == 0 && m0 + q * 32 < a.n) a.kflags_out[(m0 >> 5) + q] = qflag[q];
+            } else if (piece == 0 && part == 0 && lane == 0 && m0 + q * 32 < a.n) {
+                a.kflags_out[(m0 >> 5) + q] = 0u;
             }
         }
         tc_fence_before();
@@ -296,17 +422,19 @@ __global__ void k_dense_reduce(DenseArgs a) {
     const int row = (a.tile_base + t) * kBM + row_in;
     if (row >= a.n) return;
     const float dg = __ldg(a.deg + row);
+    bool low_nz = false;
     for (int c = blockIdx.x; c < a.W; c += gridDim.x) {
         float ax = 0.f;
         for (int p = 0; p < a.k_split; ++p)
             ax += a.partial[(static_cast<int64_t>(t) * a.k_split + p) * N * kBM + static_cast<int64_t>(c) * kBM + row_in];
-        finish_element(a, row, c, ax, dg);
+        low_nz |= finish_element(a, row, c, ax, dg);
     }
+    if (a.kflags_out && low_nz) atomicOr(a.kflags_out + (row >> 5), 1u);
 }
 
 // fp32 [n][ld] (node-major) -> member-major [W][n] fp32 + three bf16 planes
 __global__ void k_to_member_major(const float* __restrict__ X, int64_t ld, int n, int W, float* __restrict__ Xm,
-                                  float* __restrict__ Vm, int ldx, __nv_bfloat16* __restrict__ P, int ldp) {
+                                  float* __restrict__ Vm, int ldx, __nv_bfloat16* __restrict__ P, int nks, int nb) {
     __shared__ float tile[32][33];
     const int v0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -322,7 +450,7 @@ __global__ void k_to_member_major(const float* __restrict__ X, int64_t ld, int n
             Vm[static_cast<int64_t>(c) * ldx + v] = 0.f;
             __nv_bfloat16 h, m, l;
             split3(x, h, m, l);
-            const int64_t po = static_cast<int64_t>(c) * ldp + v, ps = static_cast<int64_t>(W) * ldp;
+            const int64_t po = plane_index(0, v, c, nks, nb), ps = static_cast<int64_t>(nks) * nb * 32;
             P[po] = h;
             P[ps + po] = m;
             P[2 * ps + po] = l;
@@ -345,13 +473,12 @@ __global__ void k_from_member_major(const float* __restrict__ Xm, int ldx, int n
     }
 }
 
-// dense bf16 adjacency from CSR: A[v][u] = 1 for every stored neighbour
+// dense bf16 adjacency from CSR: A[v][u] = 1 for every stored neighbour (blocked layout)
 __global__ void k_scatter_adjacency(const int* __restrict__ row_ptr, const int* __restrict__ col, int n,
-                                    __nv_bfloat16* __restrict__ A, int64_t lda) {
+                                    __nv_bfloat16* __restrict__ A, int nks) {
     const __nv_bfloat16 one = __float2bfloat16(1.f);
     for (int v = blockIdx.x; v < n; v += gridDim.x)
-        for (int k = row_ptr[v] + threadIdx.x; k < row_ptr[v + 1]; k += blockDim.x)
-            A[static_cast<int64_t>(v) * lda + col[k]] = one;
+        for (int k = row_ptr[v] + threadIdx.x; k < row_ptr[v + 1]; k += blockDim.x) A[adj_index(v, col[k], nks)] = one;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -386,7 +513,9 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
 
 template <int N>
 void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, float* partial, cudaStream_t s) {
-    constexpr int smem = kStages * (kATileBytes + 3 * N * kBK * 2) + 1024;
+    constexpr int full_ring = kStages * (kATileBytes + 3 * N * kBK * 2);
+    constexpr int skip_ring = kSkipStages * (kATileBytes + N * kBK * 2) + 2 * N * kBK * 2;
+    constexpr int smem = (full_ring > skip_ring ? full_ring : skip_ring) + 1024;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_dense_step<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -406,14 +535,14 @@ void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, f
     a.k_split = 1;
     a.partial = nullptr;
     count_launch();
-    k_dense_step<N><<<full, 192, smem, s>>>(mA, mP, a);
+    k_dense_step<N><<<full, kThreadsDense, smem, s>>>(mA, mP, a);
     if (tail > 0) {
         const int split = std::max(2, sms / tail);
         a.tile_base = full;
         a.k_split = split;
         a.partial = partial;
         count_launch();
-        k_dense_step<N><<<tail * split, 192, smem, s>>>(mA, mP, a);
+        k_dense_step<N><<<tail * split, kThreadsDense, smem, s>>>(mA, mP, a);
         count_launch();
         k_dense_reduce<N><<<dim3(std::min(a.W, 64), tail), kBM, 0, s>>>(a);
     }
@@ -423,17 +552,25 @@ void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, f
 
 size_t dense_partial_floats() { return static_cast<size_t>(148 * 2) * 256 * kBM; }
 
+int dense_nb(int W) { return W <= 64 ? 64 : (W <= 128 ? 128 : 256); }
+int dense_nks(int n) { return (n + kBK - 1) / kBK; }
+
+// bytes of the plane workspace: 2 x 3 blocked bf16 planes + 2 x K-step flags
+size_t dense_planes_bytes(int n, int W) {
+    const size_t plane = static_cast<size_t>(dense_nks(n)) * dense_nb(W) * 32;
+    return sizeof(__nv_bfloat16) * 6 * plane + sizeof(uint32_t) * 2 * static_cast<size_t>(dense_nks(n)) + 64;
+}
+
 size_t dense_adjacency_bytes(int n) {
-    const int64_t lda = (static_cast<int64_t>(n) + 7) / 8 * 8;
-    return static_cast<size_t>(lda) * n * 2;
+    const size_t tiles = static_cast<size_t>((n + kBM - 1) / kBM);
+    return tiles * kBM * static_cast<size_t>(dense_nks(n)) * 32 * 2;
 }
 
 void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s) {
-    const int64_t lda = (static_cast<int64_t>(g.n) + 7) / 8 * 8;
     cuda_check(cudaMemsetAsync(A, 0, dense_adjacency_bytes(g.n), s), "memset(A)");
     count_launch();
     k_scatter_adjacency<<<std::min(g.n, 148 * 16), 256, 0, s>>>(g.row_ptr, g.col, g.n,
-                                                                  static_cast<__nv_bfloat16*>(A), lda);
+                                                                  static_cast<__nv_bfloat16*>(A), dense_nks(g.n));
 }
 
 int dense_ldp(int n) { return (n + 7) / 8 * 8; }
@@ -444,29 +581,39 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
                           void* planes, cudaStream_t s, int col_base, float* partial) {
     const int n = g.n;
-    const int ldp = dense_ldp(n);
-    const int ldx = ldp;
+    const int ldx = dense_ldp(n);
+    const int nks = dense_nks(n);
+    // UMMA N (and the plane block height) = W rounded up to 64 / 128 / 256; the extra
+    // columns of a block stay zero and their accumulator columns are never written back
+    const int NB = dense_nb(W);
+    const size_t plane3 = static_cast<size_t>(3) * nks * NB * 32;
     __nv_bfloat16* P = static_cast<__nv_bfloat16*>(planes);
-    __nv_bfloat16* Pbuf[2] = {P, P + static_cast<size_t>(3) * W * ldp};
+    __nv_bfloat16* Pbuf[2] = {P, P + plane3};
+    cuda_check(cudaMemsetAsync(P, 0, sizeof(__nv_bfloat16) * 2 * plane3, s), "memset(planes)");
+    // K-step flags (after both plane buffers): the initial planes are never skipped
+    uint32_t* F = reinterpret_cast<uint32_t*>(P + 2 * plane3);
+    uint32_t* Fbuf[2] = {F, F + nks};
+    static const bool skip = [] {
+        const char* e = std::getenv("LCB_DENSE_SKIP");
+        return !e || std::atoi(e) != 0;
+    }();
+    cuda_check(cudaMemsetAsync(F, 1, sizeof(uint32_t) * static_cast<size_t>(nks), s), "memset(kflags)");
     const dim3 tg((n + 31) / 32, (W + 31) / 32);
     count_launch();
-    k_to_member_major<<<tg, dim3(32, 8), 0, s>>>(X_nodemajor_in, ld, n, W, Xm, Vm, ldx, Pbuf[0], ldp);
-    const int64_t lda = (static_cast<int64_t>(n) + 7) / 8 * 8;
-    // UMMA N (and the plane TMA box height) = W rounded up to 64 / 128 / 256; the extra
-    // columns read the next plane's rows (or OOB zeros) and are never written back
-    const int NB = W <= 64 ? 64 : (W <= 128 ? 128 : 256);
+    k_to_member_major<<<tg, dim3(32, 8), 0, s>>>(X_nodemajor_in, ld, n, W, Xm, Vm, ldx, Pbuf[0], nks, NB);
+    const uint64_t tiles = static_cast<uint64_t>((n + kBM - 1) / kBM);
     CUtensorMap mA, mP[2];
-    make_map(&mA, A, static_cast<uint64_t>(n), static_cast<uint64_t>(n), static_cast<uint64_t>(lda), kBK, kBM);
+    make_map(&mA, A, kBK, tiles * static_cast<uint64_t>(nks) * kBM, kBK, kBK, kBM);
     for (int b = 0; b < 2; ++b)
-        make_map(&mP[b], Pbuf[b], static_cast<uint64_t>(n), static_cast<uint64_t>(3) * W, static_cast<uint64_t>(ldp),
-                 kBK, static_cast<uint32_t>(NB));
+        make_map(&mP[b], Pbuf[b], kBK, static_cast<uint64_t>(3) * nks * NB, kBK, kBK, static_cast<uint32_t>(NB));
     DenseArgs a{};
     a.deg = g.deg32;
     a.X = Xm;
     a.V = Vm;
     a.n = n;
     a.ldx = ldx;
-    a.ldp = ldp;
+    a.nks = nks;
+    a.nb = NB;
     a.W = W;
     a.l = l;
     a.mu = mu;
@@ -479,6 +626,8 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     for (int64_t it = 0; it < iters; ++it) {
         a.it = static_cast<int>(it);
         a.planes_out = Pbuf[(it + 1) & 1];
+        a.kflags_in = skip ? Fbuf[it & 1] : nullptr;
+        a.kflags_out = skip ? Fbuf[(it + 1) & 1] : nullptr;
         const CUtensorMap& mp = mP[it & 1];
         if (NB == 64)
             launch_dense_n<64>(mA, mp, a, partial, s);
@@ -489,6 +638,14 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     }
     count_launch();
     k_from_member_major<<<tg, dim3(32, 8), 0, s>>>(Xm, ldx, n, W, X_nodemajor_out, ld);
+    if (std::getenv("LCB_DENSE_STATS")) {
+        std::vector<uint32_t> h(static_cast<size_t>(nks), 0);
+        cudaMemcpyAsync(h.data(), Fbuf[iters & 1], sizeof(uint32_t) * nks, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        int z = 0;
+        for (uint32_t c : h) z += c == 0;
+        fprintf(stderr, "dense: %d of %d K steps skippable after %lld iterations\n", z, nks, static_cast<long long>(iters));
+    }
 }
 
 }  // namespace lcb

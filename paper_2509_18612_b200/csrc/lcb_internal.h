@@ -130,6 +130,7 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
                           void* planes, cudaStream_t s, int col_base, float* partial);
 size_t dense_partial_floats();
+size_t dense_planes_bytes(int n, int W);
 // L2-panel path (lcb_narrow.cu): all iterations for one narrow column panel
 int narrow_panel_cols(int elem_bytes);
 template <typename T>

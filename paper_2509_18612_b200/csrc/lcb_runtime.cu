@@ -434,7 +434,7 @@ struct Work {
     DBuf<double> mean, dtrace, hostbatch;
     DBuf<int8_t> sign;
     DBuf<float> dXm, dVm;        // dense path: member-major iterate / velocity of one column chunk
-    DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes
+    DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes + K-step flags
     DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
     DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
     DBuf<uint64_t> bf;           // exhaustive scan: masks, upper masks, degrees, block records
@@ -596,7 +596,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                 const int Wc = std::min(256, W - c0);
                 float* Xm = w.dXm.ensure(static_cast<size_t>(Wc) * ldp);
                 float* Vm = w.dVm.ensure(static_cast<size_t>(Wc) * ldp);
-                void* P = w.dplanes.ensure(static_cast<size_t>(6) * Wc * ldp);
+                void* P = w.dplanes.ensure((dense_planes_bytes(g.n, Wc) + 1) / 2);
                 // tlim/alpha are per member; chunk boundaries are member-aligned when 256 % l == 0
                 int64_t chunk_iters = iters;
                 if (seg_iters && err_seg > 0) {  // segments in descending T: the chunk's first one is the longest

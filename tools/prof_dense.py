@@ -22,3 +22,4 @@ print(f"graph {g.node_count()} nodes {g.edge_count()} edges in {time.perf_counte
 cfg = lc.SolverConfig(batch_size=256, ascent=lc.AscentParams(0.05, a.T, 0.9, False), num_batches=1)
 out = lc.pquco(g, cfg, 0, opts=lc.RunOptions(precision=LCB_FP32, host_init=0))
 print("cut", out.best.cut_value, "ms/iteration", out.step_ms / a.T, flush=True)
+# ncu late in the run (planes skippable):  ... -k regex:k_dense_step -s 16 -c 1 python tools/prof_dense.py --T 12

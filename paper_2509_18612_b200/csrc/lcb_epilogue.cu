@@ -271,6 +271,28 @@ void launch_round_pack(const T* X, int64_t ld, int n, int members, int l, int li
     k_round_pack<T><<<blocks, 256, 0, s>>>(X, ld, n, members, l, lifted, Z, words);
 }
 
+// largest entry of a uint32 array (graph ingest: adjacency range check on the device)
+__global__ void k_max_u32(const uint32_t* __restrict__ a, int64_t count, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < count; i += stride) {
+        if (i + 3 < count && (reinterpret_cast<uintptr_t>(a + i) & 15) == 0) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + i);
+            m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
+        } else {
+            for (int64_t j = i; j < i + 4 && j < count; ++j) m = max(m, a[j]);
+        }
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+void launch_max_u32(const uint32_t* a, int64_t count, unsigned* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(unsigned), s);
+    count_launch();
+    k_max_u32<<<148 * 8, 256, 0, s>>>(a, count, out);
+}
+
 void launch_pack_bytes(const uint8_t* z, int n, int count, uint32_t* Z, cudaStream_t s) {
     const int words = (count + 31) / 32;
     count_launch();

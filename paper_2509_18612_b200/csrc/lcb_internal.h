@@ -163,6 +163,7 @@ template <typename T>
 void launch_round_pack(const T* X, int64_t ld, int n, int members, int l, int lifted,
                        uint32_t* Z, cudaStream_t s);
 void launch_pack_bytes(const uint8_t* z, int n, int count, uint32_t* Z, cudaStream_t s);
+void launch_max_u32(const uint32_t* a, int64_t count, unsigned* out, cudaStream_t s);
 // bit-sliced cut counts per member (cuts zeroed inside)
 void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts,
                       cudaStream_t s);

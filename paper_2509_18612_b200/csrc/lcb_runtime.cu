@@ -182,8 +182,14 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         if (off[v + 1] < off[v]) fail(LCB_VALIDATION, "offsets must be non-decreasing");
     const int64_t nnz = off[n];
     if (nnz > std::numeric_limits<int>::max()) fail(LCB_VALIDATION, "graph exceeds 2^31 adjacency entries");
-    for (int64_t k = 0; k < nnz; ++k)
-        if (adj[k] >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
+    // adjacency range check: on the host when the host relabelling below indexes with the
+    // entries (n <= kResidentMaxRows), else on the device right after the upload
+    const bool host_check = n <= static_cast<uint32_t>(kResidentMaxRows);
+    if (host_check) {
+        uint32_t mx = 0;  // branch-free (vectorised) scan
+        for (int64_t k = 0; k < nnz; ++k) mx = std::max(mx, adj[k]);
+        if (nnz && mx >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
+    }
     g.device = device;
     g.n = static_cast<int>(n);
     g.nnz = nnz;
@@ -222,6 +228,16 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
     // uint32 ids < n < 2^31: the same bits as int32, uploaded straight from the caller
     if (nnz) h2d(g.col, adj, sizeof(int) * nnz, 0);
+    if (!host_check && nnz) {
+        unsigned* dmx = nullptr;
+        CK(cudaMalloc(&dmx, sizeof(unsigned)));
+        launch_max_u32(reinterpret_cast<const uint32_t*>(g.col), nnz, dmx, 0);
+        unsigned mx = 0;
+        d2h(&mx, dmx, sizeof(unsigned), 0);
+        CK(cudaStreamSynchronize(0));
+        cudaFree(dmx);
+        if (mx >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
+    }
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);

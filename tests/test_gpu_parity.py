@@ -411,3 +411,16 @@ def test_l2_panel_chunked_driver_bitwise(tmp_path):
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
                        env={**os.environ, "LCB_CHUNK": "1", "LCB_RESIDENT": "0"})
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-2000:]
+
+
+def test_adjacency_range_checked_on_both_ingest_paths():
+    """Entries >= n are rejected (graph.cpp:18-21 semantics): on the host for graphs the
+    host relabels (n <= 14336), on the device after the upload for larger ones."""
+    for n in (100, 20000):
+        off = np.zeros(n + 1, dtype=np.int64)
+        off[1:] = 2
+        off[1] = 1
+        adj = np.array([1, 0], dtype=np.uint32)
+        lc.Graph.from_csr(n, off, adj).handle()  # fine
+        with pytest.raises(lc.ValidationError, match="out of range"):
+            lc.Graph.from_csr(n, off, np.array([n, 0], dtype=np.uint32)).handle()

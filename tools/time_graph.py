@@ -11,8 +11,9 @@ from paper_2509_18612_b200 import liftcut as lc  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=10000)
+ap.add_argument("--dense", action="store_true", help="config-3 graph: ER n=20k p=0.5")
 a = ap.parse_args()
-g = ba_graph(a.n, 4, 0)
+g = lc.generate_er(20_000, 0.5, 0) if a.dense else ba_graph(a.n, 4, 0)
 g.handle()
 best = 1e9
 for _ in range(5):
@@ -21,4 +22,4 @@ for _ in range(5):
     h.handle()
     best = min(best, time.perf_counter() - t)
     h.release()
-print(f"graph create n={a.n}: {best * 1e3:.2f} ms")
+print(f"graph create n={g.node_count()} nnz={len(g.adjacency)}: {best * 1e3:.2f} ms")

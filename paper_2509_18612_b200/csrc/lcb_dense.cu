@@ -373,6 +373,16 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
         const int part = (warp - 2) / 4;
         const int cbeg = part * (N / parts), cend = cbeg + N / parts;
         const int row = m0 + q * 32 + lane;
+        // while the main loop runs, pull this warp's x / v lines (one 128-byte line per
+        // column and array: 32 rows x fp32) into L2, so the epilogue's loads do not pay
+        // DRAM latency one dependent round at a time
+        if (a.k_split == 1 && m0 + q * 32 < a.n) {
+            for (int c = cbeg + lane; c < cend && c < a.W; c += 32) {
+                const int64_t o = static_cast<int64_t>(c) * a.ldx + m0 + q * 32;
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a.X + o));
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a.V + o));
+            }
+        }
         mbar_wait_sleep(&acc_bar, 0);
         tc_fence_after();
         const bool live = row < a.n;

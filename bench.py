@@ -47,7 +47,7 @@ def ba_graph(n, m, seed):
 
     G = nx.barabasi_albert_graph(n, m, seed=seed)
     e = np.array(G.edges(), dtype=np.int64)
-    return lc.Graph(n, e)
+    return _graph(n, e)
 
 
 def er_sparse(n, avg_deg, seed):
@@ -65,7 +65,18 @@ def er_sparse(n, avg_deg, seed):
     # pair index -> (u, v), u < v, row-major
     u = (n - 2 - np.floor(np.sqrt(-8.0 * idx + 4.0 * n * (n - 1) - 7) / 2.0 - 0.5)).astype(np.int64)
     v = idx + u + 1 - n * (n - 1) // 2 + (n - u) * ((n - u) - 1) // 2
-    return lc.Graph(n, np.stack([u, v], 1))
+    return _graph(n, np.stack([u, v], 1))
+
+
+def _graph(n, edges):
+    """Graph(n, edges): on the device (lcb_graph_from_edges) when a GPU is present, else
+    the host constructor; both give the same CSR (tests/test_gpu_ingest.py)."""
+    from paper_2509_18612_b200 import liftcut as lc
+    import torch
+
+    if torch.cuda.is_available():
+        return lc.Graph.from_edges_device(n, edges)
+    return lc.Graph(n, edges)
 
 
 def workload(name, nranks, precision):

@@ -51,6 +51,14 @@ int lcb_device_count(int* count);
  * (the adjacency is copied back to the host only for a per-component solve). */
 int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacency, int device,
                      lcb_graph** out);
+/* Graph(n, edges) (graph.hpp:24, graph.cpp:15-50) built on the device: validation with the
+ * reference's messages, normalise u<v, radix sort, unique, symmetrise, CSR (rows ascending).
+ * eu / ev: m endpoints (duplicates and either orientation allowed). */
+int lcb_graph_from_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t m, int device,
+                         lcb_graph** out);
+/* The CSR of a graph handle (Graph::offsets / adjacency, graph.hpp:52-57):
+ * offsets [n+1], adjacency [2m] (either may be null). */
+int lcb_graph_csr(const lcb_graph* g, int64_t* offsets, uint32_t* adjacency);
 void lcb_graph_destroy(lcb_graph* g);
 int lcb_graph_info(const lcb_graph* g, uint32_t* n, int64_t* m, int64_t* max_degree);
 

@@ -78,6 +78,8 @@ SIGNATURES = {
     "lcb_cut_values": (C.c_int, [P, P, i64, P]),
     "lcb_round_cut_batch": (C.c_int, [P, P, i32, i64, i32, P, P, P, P]),
     "lcb_brute_force_maxcut": (C.c_int, [P, i32, P, P, P]),
+    "lcb_graph_from_edges": (C.c_int, [u32, P, P, i64, C.c_int, C.POINTER(P)]),
+    "lcb_graph_csr": (C.c_int, [P, P, P]),
     "lcb_dui_init": (C.c_int, [P, u64, P]),
     "lcb_idi_init": (C.c_int, [P, f64, u64, P]),
     "lcb_lifted_init_mean": (C.c_int, [P, i32, f64, i32, u64, P]),

@@ -200,6 +200,15 @@ void cuda_check(cudaError_t e, const char* what);  // throws Failure{LCB_CUDA}
 
 int num_sms(int device);
 
+// graph ingest from an edge list on the device (lcb_ingest.cu): adjacency `col` [nnz]
+// stays on the device (caller owns it), offsets come back to the host
+struct IngestResult {
+    int* col = nullptr;
+    std::vector<int64_t> off;
+    int64_t nnz = 0;
+};
+IngestResult ingest_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t m, cudaStream_t s);
+
 // process-wide counters (bench evidence: launches and host<->device bytes)
 void count_launch(int k = 1);
 void count_h2d(size_t bytes);

@@ -175,7 +175,12 @@ void free_graph(DevGraph& g) {
     g.deg32 = nullptr;
 }
 
-void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* adj, int device) {
+// Host CSR in (lcb_graph_create), or an adjacency already built on the device by the
+// edge-list ingest (dev_col, owned from here on; `adj` is then its host copy when the
+// host relabelling below needs it, i.e. n <= kResidentMaxRows, else null).
+void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* adj, int device,
+                 int* dev_col = nullptr) {
+    if (dev_col) g.col = dev_col;  // freed with the graph, also on failure
     if (n == 0) fail(LCB_VALIDATION, "graph must have at least one node");
     if (off[0] != 0) fail(LCB_VALIDATION, "offsets[0] must be 0");
     for (uint32_t v = 0; v < n; ++v)
@@ -185,7 +190,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     // adjacency range check: on the host when the host relabelling below indexes with the
     // entries (n <= kResidentMaxRows), else on the device right after the upload
     const bool host_check = n <= static_cast<uint32_t>(kResidentMaxRows);
-    if (host_check) {
+    if (host_check && !dev_col) {
         uint32_t mx = 0;  // branch-free (vectorised) scan
         for (int64_t k = 0; k < nnz; ++k) mx = std::max(mx, adj[k]);
         if (nnz && mx >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
@@ -221,14 +226,14 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
 
     DeviceScope ds(device);
     CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));
-    CK(cudaMalloc(&g.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    if (!dev_col) CK(cudaMalloc(&g.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
     CK(cudaMalloc(&g.deg64, sizeof(double) * n));
     CK(cudaMalloc(&g.deg32, sizeof(float) * n));
     CK(cudaMalloc(&g.order, sizeof(int) * n));
     h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
     // uint32 ids < n < 2^31: the same bits as int32, uploaded straight from the caller
-    if (nnz) h2d(g.col, adj, sizeof(int) * nnz, 0);
-    if (!host_check && nnz) {
+    if (nnz && !dev_col) h2d(g.col, adj, sizeof(int) * nnz, 0);
+    if (!host_check && nnz && !dev_col) {
         unsigned* dmx = nullptr;
         CK(cudaMalloc(&dmx, sizeof(unsigned)));
         launch_max_u32(reinterpret_cast<const uint32_t*>(g.col), nnz, dmx, 0);
@@ -1674,6 +1679,44 @@ int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacen
             throw;
         }
         *out = h.release();
+    });
+}
+
+int lcb_graph_from_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t m, int device,
+                         lcb_graph** out) {
+    return guard([&] {
+        if (!out || (m > 0 && (!eu || !ev))) fail(LCB_VALIDATION, "null argument");
+        if (m < 0) fail(LCB_VALIDATION, "negative edge count");
+        DeviceScope ds(device);
+        IngestResult r = ingest_edges(n, eu, ev, m, 0);
+        auto h = std::make_unique<lcb_graph>();
+        try {
+            // the host relabelling of small graphs needs the adjacency on the host too
+            std::vector<uint32_t> hadj;
+            if (n <= static_cast<uint32_t>(kResidentMaxRows) && r.nnz) {
+                hadj.resize(static_cast<size_t>(r.nnz));
+                d2h(hadj.data(), r.col, sizeof(int) * static_cast<size_t>(r.nnz), 0);
+                CK(cudaStreamSynchronize(0));
+            }
+            int* col = r.col;
+            r.col = nullptr;
+            build_graph(h->g, n, r.off.data(), hadj.empty() ? nullptr : hadj.data(), device, col);
+        } catch (...) {
+            if (r.col) cudaFree(r.col);
+            free_graph(h->g);
+            throw;
+        }
+        *out = h.release();
+    });
+}
+
+int lcb_graph_csr(const lcb_graph* g, int64_t* offsets, uint32_t* adjacency) {
+    return guard([&] {
+        if (!g) fail(LCB_VALIDATION, "null graph");
+        const HostCSR h = fetch_csr(g->g);
+        if (offsets)
+            for (size_t v = 0; v < h.off.size(); ++v) offsets[v] = h.off[v];
+        if (adjacency && !h.adj.empty()) std::memcpy(adjacency, h.adj.data(), sizeof(uint32_t) * h.adj.size());
     });
 }
 

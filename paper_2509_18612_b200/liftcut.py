@@ -176,14 +176,16 @@ class Graph:
     def _build(n: int, e: np.ndarray):
         # graph.cpp:15-50: validate, normalise u<v, sort, dedupe, symmetrise
         if len(e):
-            bad = (e < 0) | (e >= n)
-            if bad.any():
-                i = int(np.argmax(bad.any(axis=1)))
-                raise ValidationError(
-                    f"edge endpoint out of range: ({e[i, 0]}, {e[i, 1]}) with n={n}")
+            # the first offending edge in input order decides, range before self-loop
+            rng = ((e < 0) | (e >= n)).any(axis=1)
             loops = e[:, 0] == e[:, 1]
-            if loops.any():
-                raise ValidationError(f"self-loop at node {int(e[np.argmax(loops), 0])}")
+            bad = rng | loops
+            if bad.any():
+                i = int(np.argmax(bad))
+                if rng[i]:
+                    raise ValidationError(
+                        f"edge endpoint out of range: ({e[i, 0]}, {e[i, 1]}) with n={n}")
+                raise ValidationError(f"self-loop at node {int(e[i, 0])}")
             u = np.minimum(e[:, 0], e[:, 1])
             v = np.maximum(e[:, 0], e[:, 1])
             key = np.unique(u * n + v)
@@ -197,6 +199,32 @@ class Graph:
         np.add.at(off, rows + 1, 1)
         np.cumsum(off, out=off)
         return off, np.ascontiguousarray(cols[order], dtype=np.uint32)
+
+    @classmethod
+    def from_edges_device(cls, node_count: int, edges, device: Optional[int] = None) -> "Graph":
+        """Graph(n, edges) built on the GPU (lcb_graph_from_edges: radix sort + unique +
+        symmetrise, graph.cpp:15-50); same CSR and the same errors as the constructor.
+        The device handle is kept, so the first solve does not upload again."""
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        if len(e) and (e.min() < 0 or e.max() >= 2**32):
+            i = int(np.argmax(((e < 0) | (e >= node_count)).any(axis=1)))
+            raise ValidationError(f"edge endpoint out of range: ({e[i, 0]}, {e[i, 1]}) with n={node_count}")
+        eu = np.ascontiguousarray(e[:, 0], dtype=np.uint32)
+        ev = np.ascontiguousarray(e[:, 1], dtype=np.uint32)
+        dev = default_device() if device is None else device
+        h = C.c_void_p()
+        _check(_abi.lib().lcb_graph_from_edges(int(node_count), _ptr(eu), _ptr(ev), len(e), dev, C.byref(h)))
+        m = C.c_int64()
+        _abi.lib().lcb_graph_info(h, None, C.byref(m), None)
+        off = np.zeros(int(node_count) + 1, dtype=np.int64)
+        adj = np.zeros(max(2 * m.value, 1), dtype=np.uint32)
+        st = _abi.lib().lcb_graph_csr(h, _ptr(off), _ptr(adj))
+        if st != 0:
+            _abi.lib().lcb_graph_destroy(h)
+            _check(st)
+        g = cls(int(node_count), _csr=(int(node_count), off, adj[: 2 * m.value].copy()))
+        g._handles[dev] = h
+        return g
 
     @classmethod
     def from_csr(cls, n: int, offsets, adjacency) -> "Graph":

@@ -164,3 +164,12 @@ def test_presets_mirror_reference_table():
     assert (cfg.lifted_ascent.alpha, cfg.lifted_ascent.iterations) == (0.001, 2000)
     with pytest.raises(lc.ValidationError):
         lc.apply_manual_preset(cfg, "nope")
+
+
+def test_graph_constructor_first_offending_edge_decides():
+    """graph.cpp:17-25 checks each edge in order, range before self-loop."""
+    from paper_2509_18612_b200 import liftcut as lc
+    with pytest.raises(lc.ValidationError, match="self-loop at node 2"):
+        lc.Graph(5, [[0, 1], [2, 2], [1, 9]])
+    with pytest.raises(lc.ValidationError, match=r"out of range: \(1, 9\)"):
+        lc.Graph(5, [[0, 1], [1, 9], [2, 2]])

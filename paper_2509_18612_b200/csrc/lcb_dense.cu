@@ -25,8 +25,13 @@
 // per 32-node K step, whether any mid / lo entry is nonzero; the next launch loads and
 // multiplies only the hi plane for the other K steps (adding A*0 changes nothing), and
 // when at least half the K steps skip it switches the ring to 8 narrower slots.
+// e4m3 units: an aligned pair of such K steps (64 nodes, all x = +-1 or 0) runs as
+// kind::f8f6f4 MMAs on an e4m3 copy of A (0/1) and of the hi plane (+-1): both exact in
+// e4m3, the products and their sums are integers, so the fp32 accumulator sees the same
+// values at half the operand bytes and twice the MMA rate.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -132,6 +137,23 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
            | (static_cast<uint32_t>(M >> 4) << 24);    // M >> 4
 }
 
+// kind::f8f6f4 instruction descriptor: e4m3 x e4m3 -> fp32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_e4m3(int M, int N) {
+    return (1u << 4)                                   // D format F32
+           | (0u << 7)                                 // A E4M3
+           | (0u << 10)                                // B E4M3
+           | (static_cast<uint32_t>(N >> 3) << 17)     // N >> 3
+           | (static_cast<uint32_t>(M >> 4) << 24);    // M >> 4
+}
+__device__ __forceinline__ void umma_e4m3(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n"
@@ -176,6 +198,7 @@ struct DenseArgs {
     int n;
     int ldx;                 // row pitch of X / V (elements)
     int nks;                 // 32-node K steps
+    int nks64;               // 64-node steps of the e4m3 operands
     int nb;                  // member rows per plane block (UMMA N: 64 / 128 / 256)
     int W;                   // live columns (<= 256, multiple of 16)
     int l;
@@ -190,6 +213,8 @@ struct DenseArgs {
     int tile_base;           // first M-tile of this launch
     int k_split;             // K pieces per tile (1: whole K, fused epilogue)
     float* partial;          // k_split > 1: fp32 partial sums [block][N][128]
+    uint8_t* plane8_out;        // e4m3 copy of the hi plane, blocked [64-node step][nb][64]
+    int fp8;                    // e4m3 operands available for fully corner-valued 64-node steps
     const uint32_t* kflags_in;  // [K steps] 0: the mid/lo planes of this 32-node K step are all zero
     uint32_t* kflags_out;       // the same for the planes written by this launch
 };
@@ -199,6 +224,12 @@ struct DenseArgs {
 // [128][32] blocks per (M tile, K step), so both operands stream as whole 8-16 KB runs.
 __host__ __device__ __forceinline__ int64_t plane_index(int p, int row, int c, int nks, int nb) {
     return ((static_cast<int64_t>(p) * nks + (row >> 5)) * nb + c) * 32 + (row & 31);
+}
+__host__ __device__ __forceinline__ int64_t plane8_index(int row, int c, int nb) {
+    return ((static_cast<int64_t>(row >> 6) * nb + c) << 6) + (row & 63);
+}
+__host__ __device__ __forceinline__ int64_t adj8_index(int v, int u, int nks64) {
+    return ((static_cast<int64_t>(v >> 7) * nks64 + (u >> 6)) * 128 + (v & 127)) * 64 + (u & 63);
 }
 __host__ __device__ __forceinline__ int64_t adj_index(int v, int u, int nks) {
     return ((static_cast<int64_t>(v >> 7) * nks + (u >> 5)) * 128 + (v & 127)) * 32 + (u & 31);
@@ -233,6 +264,9 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
     a.planes_out[po] = h;
     a.planes_out[ps + po] = mi;
     a.planes_out[2 * ps + po] = lo;
+    if (a.plane8_out)  // exact where it is used: only steps whose x are all +-1 / 0
+        a.plane8_out[plane8_index(row, c, a.nb)] =
+            static_cast<uint8_t>(__nv_cvt_float_to_fp8(x, __NV_SATFINITE, __NV_E4M3));
     return ((__bfloat16_as_ushort(mi) | __bfloat16_as_ushort(lo)) & 0x7fffu) != 0;
 }
 
@@ -245,7 +279,8 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
 //              few K steps that still need them.
 template <int N>
 __global__ void __launch_bounds__(kThreadsDense, 1)
-    k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP, DenseArgs a) {
+    k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP,
+                 const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmP8, DenseArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile (multiple of 512)
     constexpr int kFullSlot = kATileBytes + 3 * kPlaneTile;
@@ -279,6 +314,10 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
+        if (a.fp8) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA8)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP8)) : "memory");
+        }
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -308,6 +347,13 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
     const int S = skipmode ? kSkipStages : kStages;
     const int slot_bytes = skipmode ? kSkipSlot : kFullSlot;
     uint8_t* low = ring + kSkipStages * kSkipSlot;  // skip mode only: mid, lo tiles
+    // the unit sequence over this block's K steps, derived identically by producer and MMA:
+    // an e4m3 unit covers an aligned pair of 32-node steps whose mid / lo planes are zero
+    auto need = [&](int ks) { return !flags || ((need_low[ks >> 5] >> (ks & 31)) & 1u) != 0u; };
+    auto fp8_unit = [&](int k) {
+        const int ks = kb + k;
+        return a.fp8 && skipmode && (ks & 1) == 0 && k + 1 < nk && !need(ks) && !need(ks + 1);
+    };
 
     if (warp == 0) {
         // ---------------- TMA producer
@@ -317,13 +363,22 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
             int low_uses = 0;
-            for (int k = 0; k < nk; ++k) {
-                const int s = k % S;
+            for (int k = 0, u = 0; k < nk; ++u) {
+                const int s = u % S;
                 const int ks = kb + k;
-                if (k >= S) mbar_wait(&empty_bar[s], ((k / S) - 1) & 1);
+                if (u >= S) mbar_wait(&empty_bar[s], ((u / S) - 1) & 1);
                 uint8_t* st = ring + s * slot_bytes;
+                if (fp8_unit(k)) {
+                    // 64 nodes whose x are all +-1: e4m3 A and hi, same slot bytes as one
+                    // bf16 K step (128 x 64 B + N x 64 B)
+                    mbar_expect_tx(&full_bar[s], kATileBytes + kPlaneTile);
+                    tma_load_2d_hint(st, &tmA8, &full_bar[s], 0, (tile * a.nks64 + (ks >> 1)) * kBM, pol_a);
+                    tma_load_2d_hint(st + kATileBytes, &tmP8, &full_bar[s], 0, (ks >> 1) * N, pol_p);
+                    k += 2;
+                    continue;
+                }
                 // all-zero mid / lo planes (every x of these 32 nodes is +-1): skip them
-                const int np = (flags && !((need_low[ks >> 5] >> (ks & 31)) & 1u)) ? 1 : 3;
+                const int np = need(ks) ? 3 : 1;
                 mbar_expect_tx(&full_bar[s], kATileBytes + np * kPlaneTile);
                 tma_load_2d_hint(st, &tmA, &full_bar[s], 0, (tile * a.nks + ks) * kBM, pol_a);
                 tma_load_2d_hint(st + kATileBytes, &tmP, &full_bar[s], 0, ks * N, pol_p);
@@ -337,19 +392,33 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
                     tma_load_2d_hint(lp, &tmP, &full_bar[s], 0, (a.nks + ks) * N, pol_p);
                     tma_load_2d_hint(lp + kPlaneTile, &tmP, &full_bar[s], 0, (2 * a.nks + ks) * N, pol_p);
                 }
+                k += 1;
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16(kBM, N);
+        constexpr uint32_t idesc8 = idesc_e4m3(kBM, N);
         if (lane == 0) {
-            for (int k = 0; k < nk; ++k) {
-                const int s = k % S;
-                mbar_wait(&full_bar[s], (k / S) & 1);
+            bool first = true;
+            for (int k = 0, u = 0; k < nk; ++u) {
+                const int s = u % S;
+                mbar_wait(&full_bar[s], (u / S) & 1);
                 tc_fence_after();
                 const uint32_t st = smem_u32(ring + s * slot_bytes);
                 const int ks = kb + k;
-                const int np = (flags && !((need_low[ks >> 5] >> (ks & 31)) & 1u)) ? 1 : 3;  // as the producer
+                if (fp8_unit(k)) {  // as the producer
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {  // K = 32 e4m3 per MMA = 32 bytes
+                        umma_e4m3(tmem, umma_desc_k_sw64(st + kk * 32), umma_desc_k_sw64(st + kATileBytes + kk * 32),
+                                  idesc8, first ? 0u : 1u);
+                        first = false;
+                    }
+                    umma_commit(&empty_bar[s]);
+                    k += 2;
+                    continue;
+                }
+                const int np = need(ks) ? 3 : 1;
                 const uint32_t lp = (skipmode ? smem_u32(low) : st + kATileBytes + kPlaneTile) - kPlaneTile;
                 for (int p = 0; p < np; ++p)
 #pragma unroll
@@ -357,10 +426,12 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
                         const uint64_t da = umma_desc_k_sw64(st + kk * 32);
                         const uint32_t pb = p == 0 ? st + kATileBytes : lp + p * kPlaneTile;
                         const uint64_t db = umma_desc_k_sw64(pb + kk * 32);
-                        umma_bf16(tmem, da, db, idesc, (k | p | kk) != 0);
+                        umma_bf16(tmem, da, db, idesc, first ? 0u : 1u);
+                        first = false;
                     }
                 umma_commit(&empty_bar[s]);  // slot free once these MMAs have read it
                 if (skipmode && np == 3) umma_commit(&low_empty);
+                k += 1;
             }
             umma_commit(&acc_bar);           // accumulator complete
         }
@@ -483,12 +554,16 @@ __global__ void k_from_member_major(const float* __restrict__ Xm, int ldx, int n
     }
 }
 
-// dense bf16 adjacency from CSR: A[v][u] = 1 for every stored neighbour (blocked layout)
+// dense adjacency from CSR: A[v][u] = 1 for every stored neighbour, blocked, as bf16 (32-node
+// K steps) and as e4m3 (64-node steps; 0x38 = 1.0)
 __global__ void k_scatter_adjacency(const int* __restrict__ row_ptr, const int* __restrict__ col, int n,
-                                    __nv_bfloat16* __restrict__ A, int nks) {
+                                    __nv_bfloat16* __restrict__ A, int nks, uint8_t* __restrict__ A8, int nks64) {
     const __nv_bfloat16 one = __float2bfloat16(1.f);
     for (int v = blockIdx.x; v < n; v += gridDim.x)
-        for (int k = row_ptr[v] + threadIdx.x; k < row_ptr[v + 1]; k += blockDim.x) A[adj_index(v, col[k], nks)] = one;
+        for (int k = row_ptr[v] + threadIdx.x; k < row_ptr[v + 1]; k += blockDim.x) {
+            A[adj_index(v, col[k], nks)] = one;
+            A8[adj8_index(v, col[k], nks64)] = 0x38;
+        }
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -508,21 +583,23 @@ EncodeTiled encode_fn() {
 }
 
 void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch_elems,
-              uint32_t box_inner, uint32_t box_rows) {
+              uint32_t box_inner, uint32_t box_rows, int elem_bytes = 2) {
     EncodeTiled enc = encode_fn();
     if (!enc) throw Failure{5, "cuTensorMapEncodeTiled unavailable"};
     const cuuint64_t dims[2] = {inner, rows};
-    const cuuint64_t strides[1] = {pitch_elems * 2};
+    const cuuint64_t strides[1] = {pitch_elems * static_cast<uint64_t>(elem_bytes)};
     const cuuint32_t box[2] = {box_inner, box_rows};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+    const CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    const CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Failure{4, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r))};
 }
 
 template <int N>
-void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, float* partial, cudaStream_t s) {
+void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, const CUtensorMap& mA8, const CUtensorMap& mP8,
+                    DenseArgs a, float* partial, cudaStream_t s) {
     constexpr int full_ring = kStages * (kATileBytes + 3 * N * kBK * 2);
     constexpr int skip_ring = kSkipStages * (kATileBytes + N * kBK * 2) + 2 * N * kBK * 2;
     constexpr int smem = (full_ring > skip_ring ? full_ring : skip_ring) + 1024;
@@ -545,14 +622,14 @@ void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, f
     a.k_split = 1;
     a.partial = nullptr;
     count_launch();
-    k_dense_step<N><<<full, kThreadsDense, smem, s>>>(mA, mP, a);
+    k_dense_step<N><<<full, kThreadsDense, smem, s>>>(mA, mP, mA8, mP8, a);
     if (tail > 0) {
         const int split = std::max(2, sms / tail);
         a.tile_base = full;
         a.k_split = split;
         a.partial = partial;
         count_launch();
-        k_dense_step<N><<<tail * split, kThreadsDense, smem, s>>>(mA, mP, a);
+        k_dense_step<N><<<tail * split, kThreadsDense, smem, s>>>(mA, mP, mA8, mP8, a);
         count_launch();
         k_dense_reduce<N><<<dim3(std::min(a.W, 64), tail), kBM, 0, s>>>(a);
     }
@@ -565,22 +642,36 @@ size_t dense_partial_floats() { return static_cast<size_t>(148 * 2) * 256 * kBM;
 int dense_nb(int W) { return W <= 64 ? 64 : (W <= 128 ? 128 : 256); }
 int dense_nks(int n) { return (n + kBK - 1) / kBK; }
 
-// bytes of the plane workspace: 2 x 3 blocked bf16 planes + 2 x K-step flags
+int dense_nks64(int n) { return (n + 63) / 64; }
+
+// plane workspace: 2 x 3 blocked bf16 planes | 2 x K-step flags | 2 x e4m3 hi planes
+size_t dense_flags_offset(int n, int W) {
+    return sizeof(__nv_bfloat16) * 6 * static_cast<size_t>(dense_nks(n)) * dense_nb(W) * 32;
+}
+size_t dense_plane8_offset(int n, int W) {
+    const size_t o = dense_flags_offset(n, W) + sizeof(uint32_t) * 2 * static_cast<size_t>(dense_nks(n));
+    return (o + 127) & ~size_t(127);
+}
 size_t dense_planes_bytes(int n, int W) {
-    const size_t plane = static_cast<size_t>(dense_nks(n)) * dense_nb(W) * 32;
-    return sizeof(__nv_bfloat16) * 6 * plane + sizeof(uint32_t) * 2 * static_cast<size_t>(dense_nks(n)) + 64;
+    return dense_plane8_offset(n, W) + 2 * static_cast<size_t>(dense_nks64(n)) * dense_nb(W) * 64 + 64;
 }
 
-size_t dense_adjacency_bytes(int n) {
+// adjacency workspace: blocked bf16 [tiles][nks][128][32] | blocked e4m3 [tiles][nks64][128][64]
+size_t dense_adjacency_bf16_bytes(int n) {
     const size_t tiles = static_cast<size_t>((n + kBM - 1) / kBM);
     return tiles * kBM * static_cast<size_t>(dense_nks(n)) * 32 * 2;
+}
+size_t dense_adjacency_bytes(int n) {
+    const size_t tiles = static_cast<size_t>((n + kBM - 1) / kBM);
+    return dense_adjacency_bf16_bytes(n) + tiles * kBM * static_cast<size_t>(dense_nks64(n)) * 64;
 }
 
 void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s) {
     cuda_check(cudaMemsetAsync(A, 0, dense_adjacency_bytes(g.n), s), "memset(A)");
     count_launch();
-    k_scatter_adjacency<<<std::min(g.n, 148 * 16), 256, 0, s>>>(g.row_ptr, g.col, g.n,
-                                                                  static_cast<__nv_bfloat16*>(A), dense_nks(g.n));
+    k_scatter_adjacency<<<std::min(g.n, 148 * 16), 256, 0, s>>>(
+        g.row_ptr, g.col, g.n, static_cast<__nv_bfloat16*>(A), dense_nks(g.n),
+        static_cast<uint8_t*>(A) + dense_adjacency_bf16_bytes(g.n), dense_nks64(g.n));
 }
 
 int dense_ldp(int n) { return (n + 7) / 8 * 8; }
@@ -601,7 +692,16 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     __nv_bfloat16* Pbuf[2] = {P, P + plane3};
     cuda_check(cudaMemsetAsync(P, 0, sizeof(__nv_bfloat16) * 2 * plane3, s), "memset(planes)");
     // K-step flags (after both plane buffers): the initial planes are never skipped
-    uint32_t* F = reinterpret_cast<uint32_t*>(P + 2 * plane3);
+    uint32_t* F = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(planes) + dense_flags_offset(n, W));
+    const int nks64 = dense_nks64(n);
+    const size_t plane8 = static_cast<size_t>(nks64) * NB * 64;
+    uint8_t* P8 = static_cast<uint8_t*>(planes) + dense_plane8_offset(n, W);
+    uint8_t* P8buf[2] = {P8, P8 + plane8};
+    cuda_check(cudaMemsetAsync(P8, 0, 2 * plane8, s), "memset(planes8)");
+    static const bool fp8 = [] {
+        const char* e = std::getenv("LCB_DENSE_FP8");
+        return !e || std::atoi(e) != 0;
+    }();
     uint32_t* Fbuf[2] = {F, F + nks};
     static const bool skip = [] {
         const char* e = std::getenv("LCB_DENSE_SKIP");
@@ -612,10 +712,14 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     count_launch();
     k_to_member_major<<<tg, dim3(32, 8), 0, s>>>(X_nodemajor_in, ld, n, W, Xm, Vm, ldx, Pbuf[0], nks, NB);
     const uint64_t tiles = static_cast<uint64_t>((n + kBM - 1) / kBM);
-    CUtensorMap mA, mP[2];
+    CUtensorMap mA, mP[2], mA8, mP8[2];
     make_map(&mA, A, kBK, tiles * static_cast<uint64_t>(nks) * kBM, kBK, kBK, kBM);
     for (int b = 0; b < 2; ++b)
         make_map(&mP[b], Pbuf[b], kBK, static_cast<uint64_t>(3) * nks * NB, kBK, kBK, static_cast<uint32_t>(NB));
+    const uint8_t* A8 = static_cast<const uint8_t*>(A) + dense_adjacency_bf16_bytes(n);
+    make_map(&mA8, A8, 64, tiles * static_cast<uint64_t>(nks64) * kBM, 64, 64, kBM, 1);
+    for (int b = 0; b < 2; ++b)
+        make_map(&mP8[b], P8buf[b], 64, static_cast<uint64_t>(nks64) * NB, 64, 64, static_cast<uint32_t>(NB), 1);
     DenseArgs a{};
     a.deg = g.deg32;
     a.X = Xm;
@@ -623,6 +727,7 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     a.n = n;
     a.ldx = ldx;
     a.nks = nks;
+    a.nks64 = nks64;
     a.nb = NB;
     a.W = W;
     a.l = l;
@@ -638,13 +743,16 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
         a.planes_out = Pbuf[(it + 1) & 1];
         a.kflags_in = skip ? Fbuf[it & 1] : nullptr;
         a.kflags_out = skip ? Fbuf[(it + 1) & 1] : nullptr;
+        a.fp8 = skip && fp8 ? 1 : 0;
+        a.plane8_out = a.fp8 ? P8buf[(it + 1) & 1] : nullptr;
         const CUtensorMap& mp = mP[it & 1];
+        const CUtensorMap& mp8 = mP8[it & 1];
         if (NB == 64)
-            launch_dense_n<64>(mA, mp, a, partial, s);
+            launch_dense_n<64>(mA, mp, mA8, mp8, a, partial, s);
         else if (NB == 128)
-            launch_dense_n<128>(mA, mp, a, partial, s);
+            launch_dense_n<128>(mA, mp, mA8, mp8, a, partial, s);
         else
-            launch_dense_n<256>(mA, mp, a, partial, s);
+            launch_dense_n<256>(mA, mp, mA8, mp8, a, partial, s);
     }
     count_launch();
     k_from_member_major<<<tg, dim3(32, 8), 0, s>>>(Xm, ldx, n, W, X_nodemajor_out, ld);

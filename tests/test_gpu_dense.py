@@ -71,3 +71,37 @@ def test_dense_tensor_core_path_matches_oracle(sms):
             assert v["err"][T] <= 1e-5, (k, T, v)
         assert v["err"]["10"] <= 1e-3, (k, v)
         assert v["same"] >= 0.97 and v["d"] <= 2, (k, v)
+
+
+FP8_CODE = r"""
+import json, numpy as np
+import oracle as O
+from paper_2509_18612_b200 import liftcut as lc, LCB_FP32
+cg = O.generate_er(600, 0.5, 5)
+g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+rng = np.random.default_rng(1)
+B = 64
+x = rng.normal(0, 1e-4, B * cg.n)
+s = lc.DenseState(cg.n, 1, B); s.values[:] = x
+lc.ascend(g, s, lc.AscentParams(0.01, 60, 0.9, False), precision=LCB_FP32)
+cuts, _, best, _ = lc.round_cut_batch(g, s, lifted=False)
+print("RESULT" + json.dumps(dict(x=s.values.tolist(), cuts=cuts.tolist(), corner=float(np.mean(np.abs(s.values) == 1.0)))))
+"""
+
+
+def test_dense_e4m3_units_match_bf16_planes():
+    """Corner-valued 64-node steps run as e4m3 MMAs (A and x exact in e4m3): the states
+    match the all-bf16 run and the rounded cuts are identical."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for fp8 in ("0", "1"):
+        env = {**os.environ, "LCB_DENSE": "1", "LCB_DENSE_FP8": fp8}
+        r = subprocess.run([sys.executable, "-c", FP8_CODE], cwd=root, capture_output=True, text=True,
+                           timeout=900, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[fp8] = json.loads(r.stdout.split("RESULT", 1)[1])
+    a, b = out["0"], out["1"]
+    assert b["corner"] > 0.9  # the e4m3 units were exercised
+    assert a["cuts"] == b["cuts"]
+    import numpy as np
+    assert float(np.max(np.abs(np.array(a["x"]) - np.array(b["x"])))) <= 1e-5

@@ -99,19 +99,20 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         __nanosleep(256);
     }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
 __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                  uint64_t policy) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -213,7 +214,9 @@ struct DenseArgs {
     int tile_base;           // first M-tile of this launch
     int k_split;             // K pieces per tile (1: whole K, fused epilogue)
     float* partial;          // k_split > 1: fp32 partial sums [block][N][128]
-    uint8_t* plane8_out;        // e4m3 copy of the hi plane, blocked [64-node step][nb][64]
+    uint8_t* plane8_out;        // e4m3 copy of the hi plane, blocked [64-node step][nb][64], pre-swizzled
+    const uint8_t* plane8_in;   // the same, written by the previous iteration
+    const uint8_t* adj8;        // e4m3 adjacency, blocked [tile][64-node step][128][64], pre-swizzled
     int fp8;                    // e4m3 operands available for fully corner-valued 64-node steps
     const uint32_t* kflags_in;  // [K steps] 0: the mid/lo planes of this 32-node K step are all zero
     uint32_t* kflags_out;       // the same for the planes written by this launch
@@ -225,11 +228,18 @@ struct DenseArgs {
 __host__ __device__ __forceinline__ int64_t plane_index(int p, int row, int c, int nks, int nb) {
     return ((static_cast<int64_t>(p) * nks + (row >> 5)) * nb + c) * 32 + (row & 31);
 }
+// e4m3 operands are stored pre-swizzled: a block of 64-byte rows holds exactly the
+// SWIZZLE_64B shared-memory image (16-byte chunk j of row r at chunk j ^ ((r >> 1) & 3)),
+// so one contiguous bulk copy (no tensor map walk over 64-byte rows) lands it ready for
+// the UMMA descriptor
+__host__ __device__ __forceinline__ int sw64(int r, int b) {
+    return r * 64 + ((((b >> 4) ^ ((r >> 1) & 3)) << 4) | (b & 15));
+}
 __host__ __device__ __forceinline__ int64_t plane8_index(int row, int c, int nb) {
-    return ((static_cast<int64_t>(row >> 6) * nb + c) << 6) + (row & 63);
+    return (static_cast<int64_t>(row >> 6) * nb << 6) + sw64(c, row & 63);
 }
 __host__ __device__ __forceinline__ int64_t adj8_index(int v, int u, int nks64) {
-    return ((static_cast<int64_t>(v >> 7) * nks64 + (u >> 6)) * 128 + (v & 127)) * 64 + (u & 63);
+    return ((static_cast<int64_t>(v >> 7) * nks64 + (u >> 6)) << 13) + sw64(v & 127, u & 63);
 }
 __host__ __device__ __forceinline__ int64_t adj_index(int v, int u, int nks) {
     return ((static_cast<int64_t>(v >> 7) * nks + (u >> 5)) * 128 + (v & 127)) * 32 + (u & 31);
@@ -279,8 +289,7 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
 //              few K steps that still need them.
 template <int N>
 __global__ void __launch_bounds__(kThreadsDense, 1)
-    k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP,
-                 const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmP8, DenseArgs a) {
+    k_dense_step(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmP, DenseArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kPlaneTile = N * kBK * 2;             // bytes of one plane tile (multiple of 512)
     constexpr int kFullSlot = kATileBytes + 3 * kPlaneTile;
@@ -314,10 +323,6 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
-        if (a.fp8) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA8)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP8)) : "memory");
-        }
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -372,8 +377,10 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
                     // 64 nodes whose x are all +-1: e4m3 A and hi, same slot bytes as one
                     // bf16 K step (128 x 64 B + N x 64 B)
                     mbar_expect_tx(&full_bar[s], kATileBytes + kPlaneTile);
-                    tma_load_2d_hint(st, &tmA8, &full_bar[s], 0, (tile * a.nks64 + (ks >> 1)) * kBM, pol_a);
-                    tma_load_2d_hint(st + kATileBytes, &tmP8, &full_bar[s], 0, (ks >> 1) * N, pol_p);
+                    bulk_load_hint(st, a.adj8 + ((static_cast<int64_t>(tile) * a.nks64 + (ks >> 1)) << 13), kATileBytes,
+                                   &full_bar[s], pol_a);
+                    bulk_load_hint(st + kATileBytes, a.plane8_in + static_cast<int64_t>(ks >> 1) * N * 64, kPlaneTile,
+                                   &full_bar[s], pol_p);
                     k += 2;
                     continue;
                 }
@@ -598,8 +605,7 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
 }
 
 template <int N>
-void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, const CUtensorMap& mA8, const CUtensorMap& mP8,
-                    DenseArgs a, float* partial, cudaStream_t s) {
+void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, float* partial, cudaStream_t s) {
     constexpr int full_ring = kStages * (kATileBytes + 3 * N * kBK * 2);
     constexpr int skip_ring = kSkipStages * (kATileBytes + N * kBK * 2) + 2 * N * kBK * 2;
     constexpr int smem = (full_ring > skip_ring ? full_ring : skip_ring) + 1024;
@@ -622,14 +628,14 @@ void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, const CUtensor
     a.k_split = 1;
     a.partial = nullptr;
     count_launch();
-    k_dense_step<N><<<full, kThreadsDense, smem, s>>>(mA, mP, mA8, mP8, a);
+    k_dense_step<N><<<full, kThreadsDense, smem, s>>>(mA, mP, a);
     if (tail > 0) {
         const int split = std::max(2, sms / tail);
         a.tile_base = full;
         a.k_split = split;
         a.partial = partial;
         count_launch();
-        k_dense_step<N><<<tail * split, kThreadsDense, smem, s>>>(mA, mP, mA8, mP8, a);
+        k_dense_step<N><<<tail * split, kThreadsDense, smem, s>>>(mA, mP, a);
         count_launch();
         k_dense_reduce<N><<<dim3(std::min(a.W, 64), tail), kBM, 0, s>>>(a);
     }
@@ -712,14 +718,11 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
     count_launch();
     k_to_member_major<<<tg, dim3(32, 8), 0, s>>>(X_nodemajor_in, ld, n, W, Xm, Vm, ldx, Pbuf[0], nks, NB);
     const uint64_t tiles = static_cast<uint64_t>((n + kBM - 1) / kBM);
-    CUtensorMap mA, mP[2], mA8, mP8[2];
+    CUtensorMap mA, mP[2];
     make_map(&mA, A, kBK, tiles * static_cast<uint64_t>(nks) * kBM, kBK, kBK, kBM);
     for (int b = 0; b < 2; ++b)
         make_map(&mP[b], Pbuf[b], kBK, static_cast<uint64_t>(3) * nks * NB, kBK, kBK, static_cast<uint32_t>(NB));
     const uint8_t* A8 = static_cast<const uint8_t*>(A) + dense_adjacency_bf16_bytes(n);
-    make_map(&mA8, A8, 64, tiles * static_cast<uint64_t>(nks64) * kBM, 64, 64, kBM, 1);
-    for (int b = 0; b < 2; ++b)
-        make_map(&mP8[b], P8buf[b], 64, static_cast<uint64_t>(nks64) * NB, 64, 64, static_cast<uint32_t>(NB), 1);
     DenseArgs a{};
     a.deg = g.deg32;
     a.X = Xm;
@@ -745,14 +748,15 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
         a.kflags_out = skip ? Fbuf[(it + 1) & 1] : nullptr;
         a.fp8 = skip && fp8 ? 1 : 0;
         a.plane8_out = a.fp8 ? P8buf[(it + 1) & 1] : nullptr;
+        a.plane8_in = P8buf[it & 1];
+        a.adj8 = A8;
         const CUtensorMap& mp = mP[it & 1];
-        const CUtensorMap& mp8 = mP8[it & 1];
         if (NB == 64)
-            launch_dense_n<64>(mA, mp, mA8, mp8, a, partial, s);
+            launch_dense_n<64>(mA, mp, a, partial, s);
         else if (NB == 128)
-            launch_dense_n<128>(mA, mp, mA8, mp8, a, partial, s);
+            launch_dense_n<128>(mA, mp, a, partial, s);
         else
-            launch_dense_n<256>(mA, mp, mA8, mp8, a, partial, s);
+            launch_dense_n<256>(mA, mp, a, partial, s);
     }
     count_launch();
     k_from_member_major<<<tg, dim3(32, 8), 0, s>>>(Xm, ldx, n, W, X_nodemajor_out, ld);

@@ -181,6 +181,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // exact split of an fp32 value into three bf16 (truncating each remainder is exact:
 // x - bf16(x) is representable in fp32 and has <= 16 significant bits left)
 __device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
@@ -257,9 +264,9 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
     float* vp = a.V + static_cast<int64_t>(c) * a.ldx + row;
     float x = *xp;
     if (act) {
-        const float y = dg * x - ax;          // Lx    (graph.cpp:120)
-        const float v = a.mu * *vp + y;       // v     (ascent.cpp:68)
-        const float raw = x + alpha * v;      // raw   (ascent.cpp:69)
+        const float y = __fsub_rn(__fmul_rn(dg, x), ax);         // Lx    (graph.cpp:120)
+        const float v = __fadd_rn(__fmul_rn(a.mu, *vp), y);      // v     (ascent.cpp:68)
+        const float raw = __fadd_rn(x, __fmul_rn(alpha, v));     // raw   (ascent.cpp:69)
         if (!isfinite(raw))
             atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
                       (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
@@ -278,6 +285,66 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
         a.plane8_out[plane8_index(row, c, a.nb)] =
             static_cast<uint8_t>(__nv_cvt_float_to_fp8(x, __NV_SATFINITE, __NV_E4M3));
     return ((__bfloat16_as_ushort(mi) | __bfloat16_as_ushort(lo)) & 0x7fffu) != 0;
+}
+
+// 8 columns [c0, c0 + 8) of one row from one tcgen05.ld.x8: the x / v loads are all
+// issued before the first store, parameters and addresses are hoisted, and the member
+// index (a division) is only formed on the per-member paths.  Kept to 8 columns so the
+// epilogue loop body stays small: the fully unrolled 32-column version overflowed the
+// instruction cache ("no instruction" stalls dominated the epilogue).
+__device__ __forceinline__ bool finish_chunk8(const DenseArgs& a, int row, int c0, const uint32_t (&r)[8], float dg) {
+    const int64_t ld = a.ldx;
+    float* xr = a.X + static_cast<int64_t>(c0) * ld + row;
+    float* vr = a.V + static_cast<int64_t>(c0) * ld + row;
+    const int cn = a.W - c0 < 8 ? a.W - c0 : 8;
+    float xs[8], vs[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < cn) {
+            xs[j] = xr[j * ld];
+            vs[j] = vr[j * ld];
+        }
+    const bool uniform = !a.alpha && !a.tlim;
+    __nv_bfloat16* P = a.planes_out + plane_index(0, row, c0, a.nks, a.nb);
+    const int64_t ps = static_cast<int64_t>(a.nks) * a.nb * 32;
+    uint8_t* P8 = a.plane8_out ? a.plane8_out + (static_cast<int64_t>(row >> 6) * a.nb << 6) : nullptr;
+    const int b8 = row & 63;
+    bool low = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j >= cn) continue;
+        const int c = c0 + j;
+        float alpha = a.alpha_uniform;
+        bool act = true;
+        if (!uniform) {
+            const int m = (a.col_base + c) / a.l;
+            if (a.tlim) act = a.it < __ldg(a.tlim + m);
+            if (a.alpha) alpha = __ldg(a.alpha + m);
+        }
+        float x = xs[j];
+        if (act) {
+            const float ax = __uint_as_float(r[j]);
+            const float y = __fsub_rn(__fmul_rn(dg, x), ax);      // Lx    (graph.cpp:120)
+            const float v = __fadd_rn(__fmul_rn(a.mu, vs[j]), y); // v     (ascent.cpp:68)
+            const float raw = __fadd_rn(x, __fmul_rn(alpha, v));  // raw   (ascent.cpp:69)
+            if (!isfinite(raw)) {
+                const int m = (a.col_base + c) / a.l;
+                atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
+                          (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
+            }
+            x = raw < -1.f ? -1.f : (raw > 1.f ? 1.f : raw);  // ascent.cpp:73
+            xr[j * ld] = x;
+            vr[j * ld] = v;
+        }
+        __nv_bfloat16 h, mi, lo;
+        split3(x, h, mi, lo);
+        P[j * 32] = h;
+        P[ps + j * 32] = mi;
+        P[2 * ps + j * 32] = lo;
+        if (P8) P8[sw64(c, b8)] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(x, __NV_SATFINITE, __NV_E4M3));
+        low |= ((__bfloat16_as_ushort(mi) | __bfloat16_as_ushort(lo)) & 0x7fffu) != 0;
+    }
+    return low;
 }
 
 // Two smem carve-ups of the same ring, chosen per launch from the K-step flags of the
@@ -466,21 +533,18 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
         const bool live = row < a.n;
         const float dg = live ? __ldg(a.deg + row) : 0.f;
         bool low_nz = false;  // any nonzero mid / lo plane entry in this warp's 32 nodes
-        for (int c0 = cbeg; c0 < cend; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
+#pragma unroll 1
+        for (int c0 = cbeg; c0 < cend; c0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
             if (a.k_split > 1) {  // split-K piece: fp32 partial sums, coalesced along rows
                 float* pp = a.partial + static_cast<int64_t>(blockIdx.x) * N * kBM + q * 32 + lane;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) pp[static_cast<int64_t>(c0 + j) * kBM] = __uint_as_float(r[j]);
+                for (int j = 0; j < 8; ++j) pp[static_cast<int64_t>(c0 + j) * kBM] = __uint_as_float(r[j]);
                 continue;
             }
-            if (!live) continue;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int c = c0 + j;
-                if (c < a.W) low_nz |= finish_element(a, row, c, __uint_as_float(r[j]), dg);
-            }
+            if (!live || c0 >= a.W) continue;
+            low_nz |= finish_chunk8(a, row, c0, r, dg);
         }
         // one lane quarter = one 32-node K step of the next iteration's B operand; split-K
         // tail tiles: piece 0 clears the flag, k_dense_reduce ORs it in after the pieces

@@ -102,7 +102,8 @@ def workload(name, nranks, precision):
         cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=256,
                               ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1,
                               search=lc.auto_search_bounds())
-        desc = "BA n=100k m=4, pQUCO B=256 + evolutionary (alpha,T) search, one run per GPU"
+        desc = ("BA n=100k m=4, pQUCO B=256 + evolutionary (alpha,T) search; at N GPUs N independent "
+                "searches (seed k*N+rank), best cut reduced over ranks with NCCL")
     else:
         g = ba_graph(10_000, 4, 0)
         cfg = lc.SolverConfig(algorithm=lc.Algorithm.pDECO, batch_size=1024, lift_dim=2,
@@ -289,7 +290,11 @@ def run_b200(args):
     g, cfg, desc = workload(args.config, world, args.precision)
     # batched search rounds measured slower on config 5 (B=256 already fills the GPU; see
     # profiles/round1_kernel_ab.md), so the bench keeps the sequential evolve() order
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=comm, batched_search=False)
+    # config 5 shards independent searches: rank r runs its own solve with seed
+    # k*N + r and no member sharding; the best cut is reduced over ranks with NCCL at the end
+    independent = args.config == "c5" and world > 1
+    opts = lc.RunOptions(precision=prec, host_init=0, comm=None if independent else comm, batched_search=False)
+    seed_of = (lambda k: k * world + rank) if independent else (lambda k: k)
     solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[int(cfg.algorithm)]
     g.handle(local)  # inputs resident in HBM before timing
 
@@ -311,7 +316,7 @@ def run_b200(args):
     for k in range(args.steps):
         flush.fill_(k & 0xFF)  # L2 flush between timed steps (untimed)
         barrier()
-        out = solve(g, cfg, seed=k, opts=opts)
+        out = solve(g, cfg, seed=seed_of(k), opts=opts)
         dev_ms += out.solve_ms
         step_ms += out.step_ms
         step_bytes += out.step_bytes
@@ -333,7 +338,7 @@ def run_b200(args):
     t0 = time.perf_counter()
     for k in range(args.steps):
         gh = lc.Graph.from_csr(g.node_count(), g.offsets, g.adjacency)
-        solve(gh, cfg, seed=k, opts=opts)
+        solve(gh, cfg, seed=seed_of(k), opts=opts)
         gh.release()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -343,6 +348,10 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms, max_e2e = float(t[0]), float(t[1])
+    if world > 1:  # best cut over ranks (identical on every rank unless the runs are independent)
+        bt = torch.tensor([best], dtype=torch.int64, device=f"cuda:{local}")
+        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+        best = int(bt[0])
     total_ups = ups * world
     value = total_ups / (max_ms / 1e3)
     e2e_value = total_ups / max_e2e

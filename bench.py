@@ -227,9 +227,10 @@ def cpu_reference_step(g, cfg, nranks, t_sample, repeats=1):
 
 def ref_sample(name):
     """(T, repeats) of one bounded CPU sample: ~10-15 s of reference work on the GPU box's
-    16 host threads (measured rates: c1 1.1e9, c2 8.3e8, c3 5.0e5, c4 1.6e8, c5 3.9e8
-    node-updates/s); per-batch init / rounding stays the share it has at the full T."""
-    return {"c1": (500, 400), "c2": (50, 1), "c3": (1, 1), "c4": (4, 1), "c5": (200, 1)}[name]
+    16 host threads (measured samples: c1 400 solves 6.8 s, c2 T=50 9.6 s, c3 T=1 10.2 s,
+    c4 T=4 8.8 s, c5 T=200 5.3 s); per-batch init / rounding stays the share it has at the
+    full T."""
+    return {"c1": (500, 600), "c2": (55, 1), "c3": (1, 1), "c4": (5, 1), "c5": (400, 1)}[name]
 
 
 # ------------------------------------------------------------------ reference arm

@@ -369,9 +369,10 @@ def run_b200(args):
             roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
                     "frac": achieved / tpeak, "traffic": ncu_traffic(args.config, args.precision, kname),
                     "kernel": kname, "algorithmic_flops_per_launch": k_amount / max(k_launch, 1),
-                    "executed_tflops": 3 * achieved, "executed_frac": 3 * achieved / tpeak,
                     "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": twhich,
-                    "model": "2*n^2*W flops per iteration (SURVEY 8d); executed = 3x (bf16 hi/mid/lo planes)"}
+                    "model": "2*n^2*W algorithmic flops per iteration (SURVEY 8d). Executed MMA work differs "
+                             "per 32-node K step: bf16 hi/mid/lo planes before saturation, mid/lo skipped when "
+                             "all zero, e4m3 MMAs on corner-valued steps (DESIGN.md K3)"}
         else:
             achieved = k_amount / (k_ms / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

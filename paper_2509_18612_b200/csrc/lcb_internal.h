@@ -90,6 +90,14 @@ struct StepArgs {
     T mu;
     T alpha_uniform;            // used when alpha == nullptr
     int it;
+    // saturation codes of the iterate (K1, S = 1): one byte per (row, slab, lane), bit e set
+    // when the lane's element e is +1, bit 4+e when it is -1.  A neighbour slab whose lane
+    // elements are all on the box corners is rebuilt from its code byte (one 32-byte sector
+    // per warp) instead of gathering its 512-byte slab; the values are exactly +-1, so the
+    // CSR-order sums are unchanged bit for bit.
+    const uint8_t* sgn_in;      // codes of x_in, or nullptr (first iteration of a loop)
+    uint8_t* sgn_out;           // codes of x_out, or nullptr (not recorded)
+    int64_t sgn_ld;             // bytes per row: (ld / span) * 32
 };
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };

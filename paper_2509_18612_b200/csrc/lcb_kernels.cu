@@ -65,9 +65,32 @@ constexpr int kWarps = 8;  // warps per block of the step kernel (one row each)
 //   GEN = per-member alpha / iteration limit (batched search) or early exit
 //   EE  = early-exit bits (implies GEN)
 // ---------------------------------------------------------------------------
-template <typename T, int S, bool GEN, bool EE, int MODE>
+template <typename T>
+__device__ __forceinline__ bool sat_code(uint32_t c) {
+    constexpr uint32_t full = (1u << Vec<T>::E) - 1u;
+    return ((c | (c >> 4)) & full) == full;
+}
+// add the +-1 values of a saturated code to acc (sequential order is kept by the caller)
+__device__ __forceinline__ void add_code(float4& acc, uint32_t c) {
+    acc.x = __fadd_rn(acc.x, (c & 1u) ? 1.f : -1.f);
+    acc.y = __fadd_rn(acc.y, (c & 2u) ? 1.f : -1.f);
+    acc.z = __fadd_rn(acc.z, (c & 4u) ? 1.f : -1.f);
+    acc.w = __fadd_rn(acc.w, (c & 8u) ? 1.f : -1.f);
+}
+__device__ __forceinline__ void add_code(double2& acc, uint32_t c) {
+    acc.x = __dadd_rn(acc.x, (c & 1u) ? 1.0 : -1.0);
+    acc.y = __dadd_rn(acc.y, (c & 2u) ? 1.0 : -1.0);
+}
+
+#ifndef LCB_CODE_GROUP
+#define LCB_CODE_GROUP 8
+#endif
+constexpr int kCodeGroup = LCB_CODE_GROUP;  // neighbours whose codes load together (one dependent round)
+
+template <typename T, int S, bool GEN, bool EE, int MODE, bool REC>
 __global__ void __launch_bounds__(kWarps * 32)
     k_step(StepArgs<T> a, int groups) {
+    static_assert(!REC || (S == 1 && MODE == MODE_STEP), "saturation codes: one slab per warp, step mode");
     constexpr int E = Vec<T>::E;
     using V = typename Vec<T>::type;
     constexpr int SPAN = 32 * S * E;
@@ -97,6 +120,16 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int row = a.order ? __ldg(a.order + slot) : slot;
         const int c0 = group * SPAN + lane * E;
         const T* xin = a.x_in + c0;
+        const uint8_t* sin = REC ? a.sgn_in + group * 32 + lane : nullptr;
+#if LCB_REC_EARLY
+        // own x / v issued before the gathers: with coded gathers the kernel is latency-bound
+        V xv_early{}, vv_early{};
+        if constexpr (REC) {
+            const int64_t off0 = static_cast<int64_t>(row) * a.ld + c0;
+            xv_early = __ldcs(reinterpret_cast<const V*>(a.x_in + off0));
+            vv_early = __ldcs(reinterpret_cast<const V*>(a.vel + off0));
+        }
+#endif
 
         V acc[S];
 #pragma unroll
@@ -110,6 +143,51 @@ __global__ void __launch_bounds__(kWarps * 32)
             const int cnt = min(32, end - base);
             const int mycol = lane < cnt ? __ldg(a.col + base + lane) : 0;
             int k = 0;
+            if constexpr (REC) {
+                if (a.sgn_in) {
+                    // codes of up to 16 neighbours in one round; when every lane's elements
+                    // of all of them sit on the box corners, the sums come from the codes
+                    // alone (no slab gathers), else this group gathers as usual
+                    for (; k < cnt; k += kCodeGroup) {
+                        const int kn = min(kCodeGroup, cnt - k);
+                        uint32_t cq[kCodeGroup];
+                        bool all = true;
+#pragma unroll
+                        for (int q = 0; q < kCodeGroup; ++q) {
+                            const int u = __shfl_sync(0xffffffffu, mycol, (k + q) & 31);
+                            cq[q] = q < kn ? static_cast<uint32_t>(__ldg(sin + static_cast<int64_t>(u) * a.sgn_ld)) : 0xFFu;
+                        }
+#pragma unroll
+                        for (int q = 0; q < kCodeGroup; ++q) all = all && sat_code<T>(cq[q]);
+                        if (__all_sync(0xffffffffu, all)) {
+#pragma unroll
+                            for (int q = 0; q < kCodeGroup; ++q)
+                                if (q < kn) add_code(acc[0], cq[q]);
+                            continue;
+                        }
+                        int kk = 0;
+                        for (; kk + 4 <= kn; kk += 4) {
+                            V v[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int u = __shfl_sync(0xffffffffu, mycol, k + kk + q);
+                                v[q] = ldg_vec(reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld));
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                                for (int e = 0; e < E; ++e) el(acc[0], e) = radd(el(acc[0], e), el(v[q], e));
+                        }
+                        for (; kk < kn; ++kk) {
+                            const int u = __shfl_sync(0xffffffffu, mycol, k + kk);
+                            const V v = ldg_vec(reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld));
+#pragma unroll
+                            for (int e = 0; e < E; ++e) el(acc[0], e) = radd(el(acc[0], e), el(v, e));
+                        }
+                    }
+                    continue;
+                }
+            }
             for (; k + 4 <= cnt; k += 4) {
                 V v[4][S];
 #pragma unroll
@@ -144,7 +222,11 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int64_t off = rb + s * 32 * E;
+#if LCB_REC_EARLY
+            V xv = REC ? xv_early : *reinterpret_cast<const V*>(a.x_in + off);
+#else
             V xv = *reinterpret_cast<const V*>(a.x_in + off);
+#endif
             if constexpr (MODE == MODE_LAPLACE) {
                 V y;
 #pragma unroll
@@ -152,7 +234,11 @@ __global__ void __launch_bounds__(kWarps * 32)
                 *reinterpret_cast<V*>(a.x_out + off) = y;
                 continue;
             } else {
+#if LCB_REC_EARLY
+                V vv = REC ? vv_early : *reinterpret_cast<const V*>(a.vel + off);
+#else
                 V vv = *reinterpret_cast<const V*>(a.vel + off);
+#endif
                 V xo;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -197,6 +283,15 @@ __global__ void __launch_bounds__(kWarps * 32)
                 }
                 *reinterpret_cast<V*>(a.x_out + off) = xo;
                 *reinterpret_cast<V*>(a.vel + off) = vv;
+                if constexpr (REC) {
+                    uint32_t code = 0;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        if (el(xo, e) == T(1)) code |= 1u << e;
+                        else if (el(xo, e) == T(-1)) code |= 16u << e;
+                    }
+                    a.sgn_out[static_cast<int64_t>(row) * a.sgn_ld + group * 32 + lane] = static_cast<uint8_t>(code);
+                }
             }
         }
     }
@@ -238,7 +333,13 @@ void dispatch_s(const StepArgs<T>& a, int S, cudaStream_t st) {
         const int groups = (a.W + SPAN - 1) / SPAN;  // slabs covering the live columns
         const dim3 grid(static_cast<unsigned>(rows_blocks) * groups);
         count_launch();
-        k_step<T, SS, GEN, EE, MODE><<<grid, kWarps * 32, 0, st>>>(a, groups);
+        if constexpr (SS == 1 && MODE == MODE_STEP) {
+            if (a.sgn_out) {
+                k_step<T, SS, GEN, EE, MODE, true><<<grid, kWarps * 32, 0, st>>>(a, groups);
+                return;
+            }
+        }
+        k_step<T, SS, GEN, EE, MODE, false><<<grid, kWarps * 32, 0, st>>>(a, groups);
     };
     if (S == 1)
         go(std::integral_constant<int, 1>{});

@@ -454,6 +454,7 @@ struct Work {
     DBuf<uint64_t> mkeys, colkeys;
     DBuf<double> mean, dtrace, hostbatch;
     DBuf<int8_t> sign;
+    DBuf<uint8_t> sgn;           // K1 saturation codes, one set per X buffer
     DBuf<float> dXm, dVm;        // dense path: member-major iterate / velocity of one column chunk
     DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes + K-step flags
     DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
@@ -764,6 +765,31 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             return r;
         }
     }
+    // K1 saturation codes (StepArgs::sgn_*): written every iteration, read from the second
+    // on; one warp span (S = 1) per slab.  They pay only when the gathers miss L2: config 4
+    // (2 GB iterate) 4.44 -> 3.71 ms/iteration; with an L2-resident iterate the extra
+    // dependent code load makes K1 slower (config 5: 169.6 -> 172.8 us, config 2 W=1024:
+    // 51.2 -> 62.0 us; profiles/round1_kernel_ab.md).  LCB_SIGNREC=0 never, 1 always,
+    // default: iterate buffer larger than L2.
+    static const int signrec = [] {
+        const char* e = std::getenv("LCB_SIGNREC");
+        return e ? std::atoi(e) : -1;
+    }();
+    static const int64_t l2_bytes = [] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
+        return static_cast<int64_t>(v > 0 ? v : (126 << 20));
+    }();
+    uint8_t* codes[2] = {nullptr, nullptr};
+    const int span = step_span<T>(W);
+    const bool codes_on = signrec == 1 || (signrec != 0 && static_cast<int64_t>(g.n) * w.ld *
+                                                                   static_cast<int64_t>(sizeof(T)) > l2_bytes);
+    if (codes_on && span == 32 * static_cast<int>(16 / sizeof(T)) && w.ld % span == 0) {
+        a.sgn_ld = (w.ld / span) * 32;
+        const size_t bytes = static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld);
+        codes[0] = w.sgn.ensure(2 * bytes);
+        codes[1] = codes[0] + bytes;
+    }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;
     const int seg_cols = err_seg * l;
@@ -772,6 +798,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         a.x_in = w.X[it & 1].p;
         a.x_out = w.X[(it + 1) & 1].p;
         a.it = static_cast<int>(it);
+        a.sgn_in = it > 0 ? codes[it & 1] : nullptr;
+        a.sgn_out = codes[(it + 1) & 1];
         if (seg_iters) {  // candidates laid out by descending T: launch only the live prefix
             while (live_segs > 0 && (*seg_iters)[live_segs - 1] <= it) --live_segs;
             a.W = std::min(W, static_cast<int>(live_segs) * seg_cols);
@@ -787,6 +815,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             StepArgs<T> b = a;
             b.x_in = a.x_out;
             b.x_out = w.Y.p;
+            b.sgn_in = nullptr;
+            b.sgn_out = nullptr;
             launch_step<T>(b, false, MODE_LAPLACE, w.st);
             CK(cudaMemsetAsync(dtr, 0, sizeof(double) * members, w.st));
             launch_member_dot<T>(a.x_out, w.Y.p, g.n, W, l, w.ld, dtr, w.st);

@@ -126,6 +126,8 @@ struct ResidentArgs {
     const int* tlim;         // [members] or null
     unsigned long long* err;
     int err_seg;             // members per error slot (0: one slot)
+    int c_base;              // first column of this launch (0 unless the wave tail is split off)
+    int c_end;               // one past the last column of this launch (0: W)
 };
 bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K);
 
@@ -149,7 +151,7 @@ int brute_force_max_layers();
 size_t brute_force_scratch_bytes();
 const void* launch_brute_force(const uint64_t* masks, const uint64_t* upper, const int* deg, int n, int layers,
                                void* scratch, cudaStream_t s);
-void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);
+int launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s);  // returns launches
 
 template <typename T>
 void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lcb_internal.h"
 
@@ -264,6 +265,21 @@ __device__ __forceinline__ void row_update_any(const VT& xv, const VT& acc, VT& 
             return;
         }
     }
+    if constexpr (K == 1 && sizeof(T) == 4 && !EE) {
+        // the K=2 packed epilogue one lane at a time (same fused ops), so a column's
+        // fp32 iterate does not depend on whether its CTA holds one or two columns
+        if (packed) {
+            const float x = comp(xv, 0);
+            const float y = __fmaf_rn(static_cast<float>(dj), x, -comp(acc, 0));
+            const float v = __fmaf_rn(mu, comp(vv, 0), y);
+            const float raw = __fmaf_rn(alpha_k[0], v, x);
+            if (!isfinite(raw))
+                atomicMin(err[0], (static_cast<unsigned long long>(mem[0]) << 32) | static_cast<unsigned>(it));
+            setc(vv, 0, v);
+            setc(xo, 0, fminf(fmaxf(raw, -1.f), 1.f));
+            return;
+        }
+    }
     row_update<T, VT, K, EE>(xv, acc, vv, xo, dj, act, alpha_k, mu, mem, it, bits, err);
 }
 
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int c0 = blockIdx.x * K;
+    const int c0 = a.c_base + blockIdx.x * K;
     T* X = reinterpret_cast<T*>(a.X);
 
     T alpha_k[K];
@@ -440,7 +456,7 @@ void go(const ResidentArgs& a, cudaStream_t s) {
         attr = true;
     }
     const size_t smem = 2 * static_cast<size_t>(a.n + 1) * sizeof(VT);
-    const int ctas = (a.W + K - 1) / K;
+    const int ctas = ((a.c_end > 0 ? a.c_end : a.W) - a.c_base + K - 1) / K;
     count_launch();
     k_resident<T, K, RPT, GEN, EE, COOP><<<ctas, kThreads, smem, s>>>(a);
 }
@@ -486,13 +502,38 @@ bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K) {
     return true;
 }
 
-void launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s) {
+int launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaStream_t s) {
     if (elem_bytes == 8)
         by_mode<double, 1>(a, ee, s);
-    else if (K == 2)
-        by_mode<float, 2>(a, ee, s);
-    else
+    else if (K == 2) {
+        // Wave tail: K=2 CTAs run one per SM, so W/2 CTAs leave a partial last wave
+        // (W=1024: 512 CTAs = 3.46 waves on 148 SMs).  When the columns past the last
+        // full wave fit one K=1 wave, they run as a K=1 launch (half the SMEM traffic
+        // per CTA) instead of a mostly idle K=2 wave.
+        static const int split = [] {
+            const char* e = std::getenv("LCB_RES_SPLIT");
+            return e ? std::atoi(e) : 1;
+        }();
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int sms = num_sms(dev);
+        const int pairs = (a.W + 1) / 2;
+        const int full = (pairs / sms) * sms;
+        const int tail_cols = a.W - 2 * full;
+        if (split && !ee && full > 0 && tail_cols > 0 && tail_cols <= sms) {
+            ResidentArgs head = a;
+            head.c_end = 2 * full;
+            by_mode<float, 2>(head, ee, s);
+            ResidentArgs tail = a;
+            tail.c_base = 2 * full;
+            by_mode<float, 1>(tail, ee, s);
+            return 2;
+        } else {
+            by_mode<float, 2>(a, ee, s);
+        }
+    } else
         by_mode<float, 1>(a, ee, s);
+    return 1;
 }
 
 }  // namespace lcb

@@ -675,7 +675,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         ra.err = a.err;
         ra.err_seg = err_seg;
         CK(cudaEventRecord(w.ev0, w.st));
-        launch_resident(ra, K, ee, static_cast<int>(sizeof(T)), w.st);
+        const int res_launches = launch_resident(ra, K, ee, static_cast<int>(sizeof(T)), w.st);
         CK(cudaEventRecord(w.ev1, w.st));
         CK(cudaGetLastError());
         d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
@@ -687,12 +687,12 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
         w.step_ms += ms;
-        w.step_launches += 1;
+        w.step_launches += res_launches;
         const double bytes = static_cast<double>(iters) *
                              (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
         w.step_bytes += bytes;
         w.kstats[3] += ms;
-        w.kstats[4] += 1;
+        w.kstats[4] += res_launches;
         w.kstats[5] += bytes;
         w.node_updates += iters * static_cast<int64_t>(g.n) * W;
         w.resident_iters += iters;

@@ -509,7 +509,8 @@ int launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaS
         // Wave tail: K=2 CTAs run one per SM, so W/2 CTAs leave a partial last wave
         // (W=1024: 512 CTAs = 3.46 waves on 148 SMs).  When the columns past the last
         // full wave fit one K=1 wave, they run as a K=1 launch (half the SMEM traffic
-        // per CTA) instead of a mostly idle K=2 wave.
+        // per CTA) instead of a mostly idle K=2 wave.  With early exit a member's columns
+        // must share a CTA, so the split needs l == 1 there.
         static const int split = [] {
             const char* e = std::getenv("LCB_RES_SPLIT");
             return e ? std::atoi(e) : 1;
@@ -520,7 +521,7 @@ int launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaS
         const int pairs = (a.W + 1) / 2;
         const int full = (pairs / sms) * sms;
         const int tail_cols = a.W - 2 * full;
-        if (split && !ee && full > 0 && tail_cols > 0 && tail_cols <= sms) {
+        if (split && (!ee || a.l == 1) && full > 0 && tail_cols > 0 && tail_cols <= sms) {
             ResidentArgs head = a;
             head.c_end = 2 * full;
             by_mode<float, 2>(head, ee, s);

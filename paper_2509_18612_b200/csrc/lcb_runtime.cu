@@ -309,9 +309,12 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             // row's p-th neighbour from its remaining ones to keep that maximum low
             // (BA 10k: 4.10 -> 3.01 on average).  fp32 only: the fp64 path keeps CSR order
             // for bit-exact sums (graph.cpp:118).
-            static const bool bank_order = [] {
+            // LCB_BANK_ORDER: 0 CSR order, 1 balance the whole warp's 32 gathers over the 16
+            // bank pairs, 2 (default) balance each half-warp (rows 0-15 / 16-31 of the group:
+            // an 8-byte LDS is served per half-warp, 16 lanes x 8 B = one 128-byte wavefront).
+            static const int bank_order = [] {
                 const char* e = std::getenv("LCB_BANK_ORDER");
-                return !e || std::atoi(e) != 0;
+                return e ? std::atoi(e) : 2;
             }();
             std::vector<uint16_t> fast;
             if (bank_order) {
@@ -319,7 +322,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                 std::vector<std::vector<uint16_t>> rem(32);
                 std::vector<int> idx;
                 idx.reserve(32);
-                std::vector<int> stamp(static_cast<size_t>(n) + 1, -1);  // slot already gathered in this step
+                std::vector<int> stamp2(2 * (static_cast<size_t>(n) + 1), -1);  // slot already gathered in this step (per half)
                 int step_id = 0;
                 for (uint32_t b0 = static_cast<uint32_t>(H); b0 < n; b0 += 32) {
                     const uint32_t b1 = std::min<uint32_t>(b0 + 32, n);
@@ -332,17 +335,21 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                         L = std::max(L, d);
                     }
                     for (int p = 0; p < L; ++p, ++step_id) {
-                        int cnt[16] = {0};
+                        int cnt2[2][16] = {{0}};
                         idx.clear();
                         for (int i = 0; i < rows; ++i)
                             if (!rem[i].empty()) idx.push_back(i);
                         std::stable_sort(idx.begin(), idx.end(),
                                          [&](int x, int y) { return rem[x].size() < rem[y].size(); });
                         for (int i : idx) {
+                            const int half = bank_order == 2 ? (i >> 4) : 0;
+                            int* cnt = cnt2[half];
+                            int* stamp = stamp2.data() + static_cast<size_t>(half) * (n + 1);
+                            const int sid = step_id;
                             int bj = 0, bc = 1 << 30;
                             for (int j = 0; j < static_cast<int>(rem[i].size()); ++j) {
                                 const uint16_t u = rem[i][j];
-                                const int c = stamp[u] == step_id ? -1 : cnt[u & 15];
+                                const int c = stamp[u] == sid ? -1 : cnt[u & 15];
                                 if (c < bc) {
                                     bc = c;
                                     bj = j;
@@ -352,7 +359,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                             rem[i].erase(rem[i].begin() + bj);
                             fast[static_cast<size_t>(rrp[b0 + i] + p)] = u;
                             if (bc >= 0) {
-                                stamp[u] = step_id;
+                                stamp[u] = sid;
                                 ++cnt[u & 15];
                             }
                         }

@@ -34,20 +34,21 @@ off = np.cumsum(off)
 g = lc.Graph.from_csr(n, off, a[:, 1].astype(np.uint32))
 s = lc.DenseState(n, 1, B)
 s.values[:] = rng.uniform(-1e-2, 1e-2, s.values.shape)
-lc.ascend(g, s, lc.AscentParams(0.05, T, 0.9, False), precision=LCB_FP32)
+lc.ascend(g, s, lc.AscentParams(0.05, T, 0.9, sys.argv[2] == '1'), precision=LCB_FP32)
 assert np.all(np.abs(s.values) <= 1.0)
 print(hashlib.sha256(np.ascontiguousarray(s.values).tobytes()).hexdigest())
 """
 
 
-def _run(split: str) -> str:
+def _run(split: str, ee: bool) -> str:
     env = dict(os.environ, LCB_RES_SPLIT=split, LCB_RESIDENT="1")
-    out = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True,
+    out = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, "1" if ee else "0"], env=env, capture_output=True, text=True,
                          timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     return out.stdout.strip().splitlines()[-1]
 
 
 @pytest.mark.gpu
-def test_resident_wave_tail_split_bitwise():
-    assert _run("1") == _run("0")
+@pytest.mark.parametrize("ee", [False, True])
+def test_resident_wave_tail_split_bitwise(ee):
+    assert _run("1", ee) == _run("0", ee)

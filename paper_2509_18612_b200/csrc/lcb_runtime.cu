@@ -184,7 +184,7 @@ void free_graph(DevGraph& g) {
 // Groups are independent, so they are refined on several host threads.
 // BA 10k model (light rows): greedy 10080 -> 8307 wavefronts per iteration.
 static void refine_bank_order(std::vector<uint16_t>& fast, const std::vector<int64_t>& rrp, uint32_t H,
-                              uint32_t n) {
+                              uint32_t n, int passes) {
     const uint32_t groups = (n - H + 31) / 32;
     if (groups == 0) return;
     auto work = [&](uint32_t g0, uint32_t stride) {
@@ -237,7 +237,7 @@ static void refine_bank_order(std::vector<uint16_t>& fast, const std::vector<int
                 for (int p = 0; p < Li; ++p) add(hs[2 * p + (i >> 4)], fast[static_cast<size_t>(rrp[b0 + i] + p)]);
             }
             for (auto& x : hs) x.c = cost(x.bank);
-            for (int pass = 0; pass < 2; ++pass) {
+            for (int pass = 0; pass < passes; ++pass) {
                 bool changed = false;
                 for (int i = 0; i < rows; ++i) {
                     const int h = i >> 4;
@@ -477,11 +477,12 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                     }
                 }
             }
-            static const bool refine = [] {
+            static const int refine_passes = [] {  // LCB_BANK_REFINE = max passes, 0 disables
                 const char* e = std::getenv("LCB_BANK_REFINE");
-                return !e || std::atoi(e) != 0;
+                return e ? std::max(0, std::atoi(e)) : 2;
             }();
-            if (!fast.empty() && refine && bank_order == 2) refine_bank_order(fast, rrp, static_cast<uint32_t>(H), n);
+            if (!fast.empty() && refine_passes > 0 && bank_order == 2)
+                refine_bank_order(fast, rrp, static_cast<uint32_t>(H), n, refine_passes);
             CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * info.size()));
             CK(cudaMalloc(&g.res_chunk, sizeof(int) * chunks));
             CK(cudaMalloc(&g.res_heavy, sizeof(int) * hinfo.size()));

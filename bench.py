@@ -1,25 +1,37 @@
 #!/usr/bin/env python
 """Benchmark: PGA node-updates/s (n * B * l * iters / s) and best cut — BASELINE.json.
 
-Default workload (N=1): BASELINE.json configs[1] — Barabasi-Albert n=10k m=4
-(networkx, seed 0), B=1024 initialisations per GPU, full pDECO: 2 alternations x
-(3 unlifted batches + 3 lifted batches, l=2), T=500 each, alpha=0.05, mu=0.9, IDI,
-early exit off (work counted with early_exit=false on both sides).
-One step = one full pDECO solve = 9.216e10 node-updates per GPU.
+Headline (default, N=1): BASELINE.json config 4 — sparse ER n=1M, average degree 10
+(networkx fast_gnp_random_graph(n, 10/(n-1), seed 0), m = 4,999,707), B=512
+initialisations per GPU, pQUCO, T=500, alpha=0.05, mu=0.9, IDI, early exit off (BASELINE.md:
+work counted with early_exit=false on both sides), fp32.  The largest single-GPU
+configuration and the one BASELINE shards over 1/2/4/8 GPUs.  One step = one full
+solve = 2.56e11 node-updates per GPU.
 
-N>1 (torchrun, one process per GPU): members are sharded (rank r owns global
-members [r*B, (r+1)*B)), so the job is the reference's solve with batch 1024*N;
-per batch one NCCL allreduce(max) of the packed (cut, member) key and one of the
-winner bits.  Weak scaling.
+N>1 (one process per GPU; without WORLD_SIZE, `--gpus N` launches torch.distributed.run
+itself): members are sharded (rank r owns global members [r*B, (r+1)*B)), so the job is
+the reference's solve with batch 512*N; per batch one NCCL allreduce(max) of the packed
+(cut, member) key and one of the winner bits.  Weak scaling.
+
+At N=1 the same JSON line also carries `extra_configs`: configs 2, 3, 5 (fp32) and the
+headline in fp64 (the bit-exact mode), each measured in this run with fewer steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config c2|c1|c4|c5] [--precision fp32|fp64]
+                  [--config c4|c1|c2|c3|c5] [--precision fp32|fp64] [--no-extras]
+
+`--impl reference` times the reference's own CPU solver (oracle/_ref: the unmodified
+/root/reference sources compiled in-tree) on the host cores, on a bounded T sample of the
+same workload; its process never imports the B200 package (graphs from the same
+generators through the reference's constructor / generate_er).
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import random
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,93 +45,113 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PGA node-updates/s (n*B*iters/s) and best cut value at 1/2/4/8 B200"
 UNIT = "node-updates/s"
+DEFAULT_CONFIG = "c4"
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-# ------------------------------------------------------------------ workloads
-def ba_graph(n, m, seed):
+# ------------------------------------------------------------------ graphs (no product import)
+def fast_gnp_edges(n, p, seed):
+    """networkx.fast_gnp_random_graph(n, p, seed) (Batagelj-Brandes skipping), vectorised:
+    the same Mersenne-Twister stream as random.Random(seed), the same math.log and the same
+    truncation, so the edge set is identical (checked against networkx in
+    tests/test_bench_cpu.py); the skip sum is the linear index of pair (v, w), w < v."""
+    rng = random.Random(seed)
+    st = rng.getstate()[1]
+    rs = np.random.RandomState()
+    rs.set_state(("MT19937", np.array(st[:624], dtype=np.uint32), st[624]))
+    lp = math.log(1.0 - p)
+    total = n * (n - 1) // 2
+    out, L = [], -1
+    chunk = int(total * p * 1.05) + 1024
+    while True:
+        r = rs.random_sample(chunk)
+        lr = np.fromiter((math.log(x) for x in (1.0 - r)), dtype=np.float64, count=chunk)
+        idx = L + np.cumsum(1 + np.floor(lr / lp).astype(np.int64))
+        L = int(idx[-1])
+        done = idx >= total
+        if done.any():
+            out.append(idx[: int(np.argmax(done))])
+            break
+        out.append(idx)
+    idx = np.concatenate(out)
+    v = np.floor((1.0 + np.sqrt(1.0 + 8.0 * idx.astype(np.float64))) / 2.0).astype(np.int64)
+    v -= (v * (v - 1) // 2 > idx)
+    v += ((v + 1) * v // 2 <= idx)
+    return v, idx - v * (v - 1) // 2
+
+
+def ba_edges(n, m, seed):
     import networkx as nx
 
-    from paper_2509_18612_b200 import liftcut as lc
-
-    G = nx.barabasi_albert_graph(n, m, seed=seed)
-    e = np.array(G.edges(), dtype=np.int64)
-    return _graph(n, e)
+    e = np.array(nx.barabasi_albert_graph(n, m, seed=seed).edges(), dtype=np.int64)
+    return e[:, 0], e[:, 1]
 
 
-def er_sparse(n, avg_deg, seed):
-    """G(n, p) with p = avg_deg/(n-1), geometric skipping (numpy; networkx
-    fast_gnp_random_graph's method) — for config 4."""
-    from paper_2509_18612_b200 import liftcut as lc
+# ------------------------------------------------------------------ workloads
+# lcb_config fields (SolverConfig defaults: IDI beta 0.2, eta 0.8, init_scale 1e4)
+BASE = dict(algorithm=0, lift_dim=2, batch_size=64, num_batches=1, alpha=0.05, iterations=500, momentum=0.9,
+            early_exit=0, has_lifted_ascent=0, l_alpha=0.05, l_iterations=500, l_momentum=0.9, l_early_exit=0,
+            init_method=1, beta=0.2, eta=0.8, init_scale=1e4, init_seed=0, resample_idi=1, scale_noise=1,
+            time_budget_s=0.0, has_search=0, population_size=6, t_lower=3000, t_upper=10000, e_lower=-4.0,
+            e_upper=-1.0, rounds=5, search_refresh=0, deco_alternations=2, deco_carry=0)
 
-    rng = np.random.default_rng(seed)
-    p = avg_deg / (n - 1)
-    total = n * (n - 1) // 2
-    k = int(total * p * 1.2) + 1000
-    gaps = rng.geometric(p, size=k).astype(np.int64)
-    idx = np.cumsum(gaps) - 1
-    idx = idx[idx < total]
-    # pair index -> (u, v), u < v, row-major
-    u = (n - 2 - np.floor(np.sqrt(-8.0 * idx + 4.0 * n * (n - 1) - 7) / 2.0 - 0.5)).astype(np.int64)
-    v = idx + u + 1 - n * (n - 1) // 2 + (n - u) * ((n - u) - 1) // 2
-    return _graph(n, np.stack([u, v], 1))
-
-
-def _graph(n, edges):
-    """Graph(n, edges): on the device (lcb_graph_from_edges) when a GPU is present, else
-    the host constructor; both give the same CSR (tests/test_gpu_ingest.py)."""
-    from paper_2509_18612_b200 import liftcut as lc
-    import torch
-
-    if torch.cuda.is_available():
-        return lc.Graph.from_edges_device(n, edges)
-    return lc.Graph(n, edges)
-
-
-def workload(name, nranks, precision):
-    from paper_2509_18612_b200 import liftcut as lc
-
-    if name == "c1":
-        g = lc.generate_er(800, 0.015, 0)
-        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=64,
-                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1)
-        desc = "ER n=800 p=0.015 seed0 (ref generator), pQUCO B=64, T=500, 1 batch"
-    elif name == "c3":
-        g = lc.generate_er(20_000, 0.5, 0)
-        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=256,
-                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1)
-        desc = "dense ER n=20k p=0.5 (ref generator, ~1e8 edges), pQUCO B=256, T=500, tensor-core path"
-    elif name == "c4":
-        g = er_sparse(1_000_000, 10.0, 0)
-        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=512 // nranks if nranks > 1 else 512,
-                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1)
-        desc = "sparse ER n=1M avg deg 10, pQUCO B=512 global, T=500, 1 batch"
-    elif name == "c5":
-        g = ba_graph(100_000, 4, 0)
-        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pQUCO, batch_size=256,
-                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=1,
-                              search=lc.auto_search_bounds())
-        desc = ("BA n=100k m=4, pQUCO B=256 + evolutionary (alpha,T) search; at N GPUs N independent "
-                "searches (seed k*N+rank), best cut reduced over ranks with NCCL")
-    else:
-        g = ba_graph(10_000, 4, 0)
-        cfg = lc.SolverConfig(algorithm=lc.Algorithm.pDECO, batch_size=1024, lift_dim=2,
-                              ascent=lc.AscentParams(0.05, 500, 0.9, False), num_batches=3,
-                              deco_alternations=2)
-        desc = ("Barabasi-Albert n=10k m=4 (networkx seed 0), B=1024/GPU, full pDECO "
-                "(2 x [3 quco + 3 luco l=2 batches]), T=500, IDI, early exit off")
-    return g, cfg, desc
+WORKLOADS = {
+    "c1": dict(graph=("er_ref", 800, 0.015, 0), cfg=dict(batch_size=64),
+               desc="ER n=800 p=0.015 seed 0 (reference generate_er), pQUCO B=64/GPU, T=500, 1 batch"),
+    "c2": dict(graph=("ba", 10_000, 4, 0),
+               cfg=dict(algorithm=2, batch_size=1024, lift_dim=2, num_batches=3, deco_alternations=2),
+               desc="Barabasi-Albert n=10k m=4 (networkx seed 0), B=1024/GPU, full pDECO "
+                    "(2 x [3 quco + 3 luco l=2 batches]), T=500, IDI, early exit off"),
+    "c3": dict(graph=("er_ref", 20_000, 0.5, 0), cfg=dict(batch_size=256),
+               desc="dense ER n=20k p=0.5 seed 0 (reference generate_er, ~1e8 edges), pQUCO B=256/GPU, T=500, "
+                    "tensor-core path"),
+    "c4": dict(graph=("gnp", 1_000_000, 10.0 / 999_999, 0), cfg=dict(batch_size=512),
+               desc="sparse ER n=1M avg degree 10 (networkx fast_gnp_random_graph seed 0, m=4,999,707), "
+                    "pQUCO B=512/GPU, T=500, IDI, early exit off, 1 batch"),
+    "c5": dict(graph=("ba", 100_000, 4, 0), cfg=dict(batch_size=256, has_search=1),
+               desc="BA n=100k m=4 (networkx seed 0), pQUCO B=256 + evolutionary (alpha, T) search "
+                    "(auto bounds: T in [3000, 10000], pop 6, 5 rounds); one independent run per GPU per step "
+                    "(seed = step*N + rank), best cut reduced over ranks"),
+}
 
 
-def expected_updates(g, cfg) -> int:
-    n, B, T = g.node_count(), cfg.batch_size, cfg.ascent.iterations
-    if cfg.algorithm == 2:
-        return n * T * cfg.num_batches * cfg.deco_alternations * (B + B * cfg.lift_dim)
-    l = cfg.lift_dim if cfg.algorithm == 1 else 1
-    return n * T * cfg.num_batches * B * l
+def solver_fields(name):
+    d = dict(BASE)
+    d.update(WORKLOADS[name]["cfg"])
+    return d
+
+
+def graph_edges(name):
+    kind, *a = WORKLOADS[name]["graph"]
+    if kind == "gnp":
+        return a[0], fast_gnp_edges(*a)
+    if kind == "ba":
+        return a[0], ba_edges(*a)
+    raise ValueError(kind)
+
+
+def config_dict(name, world, precision):
+    """The `config` object of the JSON line — identical for both arms."""
+    f = solver_fields(name)
+    n = WORKLOADS[name]["graph"][1]
+    l = f["lift_dim"] if f["algorithm"] else 1
+    return {"workload": WORKLOADS[name]["desc"], "config_id": name, "precision": precision,
+            "graph_nodes": n, "members_per_gpu": f["batch_size"], "global_batch": f["batch_size"] * world,
+            "lift_dim": l, "iterations": f["iterations"],
+            "parallelism": f"member-sharded dp{world}" if world > 1 and name != "c5" else
+            (f"independent runs x{world}" if world > 1 else "single GPU"),
+            "l2": "flushed between timed steps (512 MB write); each step is a full solve"}
+
+
+def expected_updates(f, n) -> int:
+    B, T = f["batch_size"], f["iterations"]
+    if f["algorithm"] == 2:
+        return n * T * f["num_batches"] * f["deco_alternations"] * (B + B * f["lift_dim"])
+    l = f["lift_dim"] if f["algorithm"] == 1 else 1
+    return n * T * f["num_batches"] * B * l
 
 
 # ------------------------------------------------------------------ helpers
@@ -194,43 +226,42 @@ def ncu_traffic(config, precision, kernel):
     return e.get("dram_bytes_per_launch") if e else None
 
 
-def cpu_reference_step(g, cfg, nranks, t_sample, repeats=1):
-    """The reference's own CPU solve (oracle/_ref, unmodified liftcut compiled from
-    /root/reference) on the same graph and config, T reduced to t_sample (or the full
-    solve repeated `repeats` times for tiny configs), all host threads.
-    Returns (node-updates, seconds, best cut, threads)."""
+def ref_sample(name):
+    """(T, repeats) of one bounded CPU step: a few seconds of reference ascent on the GPU
+    box's host cores (c1: whole solves, c3: 1 iteration of the 1e8-edge graph)."""
+    return {"c1": (500, 40), "c2": (20, 1), "c3": (1, 1), "c4": (2, 1), "c5": (200, 1)}[name]
+
+
+def cpu_reference_step(rg, name, world, T, reps, threads):
+    """The reference's own solve (oracle/_ref: unmodified liftcut) on the same graph and
+    config, T reduced to the sample, all host threads, no search.  Returns (node-updates,
+    StageTimes.ascent_s, solve seconds, best cut)."""
     import oracle as O
 
-    rg = O.RefGraph.from_csr(O.CSR(g.node_count(), g.offsets, g.adjacency))
-    c = cfg.to_abi()
-    cc = O.default_config()
-    for f, _ in O.Config._fields_:
-        setattr(cc, f, getattr(c, f))
-    cc.batch_size = cfg.batch_size * nranks
-    cc.iterations = t_sample
-    cc.l_iterations = t_sample
-    cc.has_search = 0
-    threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    best = 0
-    for rep in range(repeats):
-        best = max(best, O.ref_solve(rg, cc, rep, workers=threads).cut_value)
-    dt = time.perf_counter() - t0
-    from copy import deepcopy
-
-    cfg2 = deepcopy(cfg)
-    cfg2.batch_size = cfg.batch_size * nranks
-    cfg2.ascent.iterations = t_sample
-    cfg2.search = None
-    return expected_updates(g, cfg2) * repeats, dt, best, threads
+    f = solver_fields(name)
+    f["batch_size"] *= world
+    f["iterations"] = f["l_iterations"] = T
+    f["has_search"] = 0
+    cc = O.default_config(**f)
+    ups, asc, sec, best = 0, 0.0, 0.0, 0
+    for rep in range(reps):
+        t0 = time.perf_counter()
+        r = O.ref_solve(rg, cc, rep, workers=threads)
+        sec += time.perf_counter() - t0
+        asc += r.stage_times["ascent_s"]
+        best = max(best, r.cut_value)
+        ups += expected_updates(f, rg.n)
+    return ups, asc, sec, best
 
 
-def ref_sample(name):
-    """(T, repeats) of one bounded CPU sample: ~10-15 s of reference work on the GPU box's
-    16 host threads (measured samples: c1 400 solves 6.8 s, c2 T=50 9.6 s, c3 T=1 10.2 s,
-    c4 T=4 8.8 s, c5 T=200 5.3 s); per-batch init / rounding stays the share it has at the
-    full T."""
-    return {"c1": (500, 600), "c2": (55, 1), "c3": (1, 1), "c4": (5, 1), "c5": (400, 1)}[name]
+def reference_graph(name):
+    import oracle as O
+
+    kind, *a = WORKLOADS[name]["graph"]
+    if kind == "er_ref":
+        return O.RefGraph.er(*a)
+    n, (u, v) = graph_edges(name)
+    return O.RefGraph.from_edges(n, u, v)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -241,41 +272,181 @@ def run_reference(args):
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libliftcut_ref.so")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libliftcut_ref.so not built"}))
         return 0
-    g, cfg, desc = workload(args.config, args.gpus, args.precision)
+    assert "paper_2509_18612_b200" not in sys.modules
+    world = args.gpus
+    rg = reference_graph(args.config)
     T, reps = ref_sample(args.config)
+    threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_reference_step(g, cfg, args.gpus, 1)  # cache warm-up only
-    ups, secs, best = 0, 0.0, 0
-    threads = 1
+        cpu_reference_step(rg, args.config, world, 1, 1, threads)  # page-in / cache warm-up only
+    ups, asc, sec, best = 0, 0.0, 0.0, 0
     for _ in range(args.steps):
-        u, dt, cut, threads = cpu_reference_step(g, cfg, args.gpus, T, reps)
-        ups += u
-        secs += dt
-        best = max(best, cut)
-    value = ups / secs
-    sample = (f"reference pDECO/pQUCO solve with T={T} (of {cfg.ascent.iterations}), global batch "
-              f"{cfg.batch_size * args.gpus}" + (f", {reps} solves per step" if reps > 1 else ""))
+        u, a, s, b = cpu_reference_step(rg, args.config, world, T, reps, threads)
+        ups, asc, sec, best = ups + u, asc + a, sec + s, max(best, b)
+    assert "paper_2509_18612_b200" not in sys.modules
+    value = ups / asc
+    f = solver_fields(args.config)
+    sample = (f"unmodified reference solve (oracle/_ref, compiled from /root/reference) with T={T} instead of "
+              f"{f['iterations']}, global batch {f['batch_size'] * world}, no search"
+              + (f", {reps} solves per step" if reps > 1 else "")
+              + f", {threads} host threads; value = node-updates / StageTimes.ascent_s "
+                f"({asc:.1f} s of {sec:.1f} s solve wall; solve-wall rate {ups / sec:.3e})")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "best_cut": best,
-        "config": {"workload": desc + f" [reference CPU sample: T={T}" + (f" x {reps} solves" if reps > 1 else "") + "]", "graph_nodes": g.node_count(),
-                   "graph_edges": g.edge_count()},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * asc / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "best_cut_sample": best, "config": config_dict(args.config, world, args.precision),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
 
 
 # ------------------------------------------------------------------ B200 arm
+class Arm:
+    def __init__(self, world, rank, local, comm):
+        self.world, self.rank, self.local, self.comm = world, rank, local, comm
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+
+    def allreduce_max(self, vals, dtype):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor(vals, dtype=getattr(torch, dtype), device=f"cuda:{self.local}")
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+
+def product_config(lc, f):
+    a = lc.AscentParams(f["alpha"], f["iterations"], f["momentum"], bool(f["early_exit"]))
+    la = (lc.AscentParams(f["l_alpha"], f["l_iterations"], f["l_momentum"], bool(f["l_early_exit"]))
+          if f["has_lifted_ascent"] else None)
+    init = lc.InitConfig(lc.InitMethod(f["init_method"]), f["beta"], f["eta"], f["init_scale"], f["init_seed"],
+                         bool(f["resample_idi"]), bool(f["scale_noise"]))
+    search = (lc.SearchConfig(f["t_lower"], f["t_upper"], f["e_lower"], f["e_upper"], f["population_size"],
+                              f["rounds"]) if f["has_search"] else None)
+    return lc.SolverConfig(lc.Algorithm(f["algorithm"]), f["batch_size"], f["lift_dim"], a, la, init,
+                           f["num_batches"], None, search, f["search_refresh"], f["deco_alternations"],
+                           lc.DecoCarry(f["deco_carry"]))
+
+
+def device_graph(lc, name, device):
+    kind, *a = WORKLOADS[name]["graph"]
+    if kind == "er_ref":
+        return lc.generate_er_device(*a, device=device)
+    n, (u, v) = graph_edges(name)
+    return lc.Graph.from_edges_device(n, np.stack([u, v], 1), device)
+
+
+KERNELS = ("k_step", "k_resident", "k_dense_step", "k_stream")
+
+
+def measure(arm, name, precision, steps, warmup, flush, with_e2e):
+    import torch  # noqa: F401
+
+    from paper_2509_18612_b200 import LCB_FP32, LCB_FP64
+    from paper_2509_18612_b200 import liftcut as lc
+
+    prec = LCB_FP32 if precision == "fp32" else LCB_FP64
+    f = solver_fields(name)
+    cfg = product_config(lc, f)
+    g = device_graph(lc, name, arm.local)
+    independent = name == "c5"  # independent searches per rank
+    opts = lc.RunOptions(precision=prec, host_init=0, comm=None if independent else arm.comm,
+                         batched_search=False)
+    seed_of = (lambda k: k * arm.world + arm.rank) if independent else (lambda k: k)
+    solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[f["algorithm"]]
+    g.handle(arm.local)  # inputs resident in HBM before timing
+    if independent:  # warm-up without the search (one search solve is ~10 s)
+        wcfg = product_config(lc, {**f, "has_search": 0, "iterations": 50})
+        for _ in range(warmup):
+            solve(g, wcfg, seed=0, opts=opts)
+    else:
+        for _ in range(warmup):
+            solve(g, cfg, seed=0, opts=opts)
+    arm.barrier()
+    l0 = lc.counters()[0]
+    dev_ms, step_ms, ups, best = 0.0, 0.0, 0, 0
+    kst = {k: [0.0, 0.0, 0.0] for k in KERNELS}
+    for k in range(steps):
+        flush.fill_(k & 0xFF)  # L2 flush between timed steps (untimed)
+        arm.barrier()
+        out = solve(g, cfg, seed=seed_of(k), opts=opts)
+        dev_ms += out.solve_ms
+        step_ms += out.step_ms
+        for kname, vals in out.kernel_stats.items():
+            for i in range(3):
+                kst[kname][i] += vals[i]
+        ups += out.node_updates
+        best = max(best, out.best.cut_value)
+        if lc.cut_value(g, out.best.assignment) != out.best.cut_value:
+            raise RuntimeError("reported cut does not recompute")
+    arm.barrier()
+    launches = lc.counters()[0] - l0
+
+    e2e_s, h2d, d2h = None, 0, 0
+    if with_e2e:  # the public API with HOST buffers (graph upload + assignment download inside)
+        h0, d0 = lc.counters()[1:]
+        arm.barrier()
+        t0 = time.perf_counter()
+        for k in range(steps):
+            gh = lc.Graph.from_csr(g.node_count(), g.offsets, g.adjacency)
+            solve(gh, cfg, seed=seed_of(k), opts=opts)
+            gh.release()
+        arm.barrier()
+        e2e_s = time.perf_counter() - t0
+        h1, d1 = lc.counters()[1:]
+        h2d, d2h = (h1 - h0) // steps, (d1 - d0) // steps
+
+    mx = arm.allreduce_max([dev_ms, e2e_s or 0.0], "float64")
+    best = int(arm.allreduce_max([best], "int64")[0]) if arm.world > 1 else best
+    total_ups = ups * arm.world
+    res = {"value": total_ups / (mx[0] / 1e3), "ms_per_step": mx[0] / steps, "best_cut": best,
+           "node_updates_per_step": total_ups // steps, "gpu_launches": launches,
+           "graph_nodes": g.node_count(), "graph_edges": g.edge_count(), "dtype": "f32" if prec == LCB_FP32 else "f64"}
+    if e2e_s is not None:
+        res["e2e"] = {"value": total_ups / mx[1], "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    res["roofline"] = roofline(kst, step_ms, name, precision)
+    g.release()
+    return res
+
+
+def roofline(kst, step_ms, name, precision):
+    kname = max(kst, key=lambda k: kst[k][0])
+    k_ms, k_launch, k_amount = kst[kname]
+    shares = {k: v[0] / max(step_ms, 1e-9) for k, v in kst.items() if v[1]}
+    if kname == "k_dense_step":
+        tpeak, twhich = measured_tensor_peak()
+        achieved = k_amount / (k_ms / 1e3) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak,
+                "traffic": ncu_traffic(name, precision, kname), "kernel": kname,
+                "algorithmic_flops_per_launch": k_amount / max(k_launch, 1),
+                "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": twhich,
+                "model": "2*n^2*W algorithmic flops per iteration (SURVEY 8d). Executed MMA work differs per "
+                         "32-node K step: bf16 hi/mid/lo planes before saturation, mid/lo skipped when all zero, "
+                         "e4m3 MMAs on corner-valued steps (DESIGN.md K3)"}
+    peak, which = measured_peaks()
+    achieved = k_amount / (k_ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(name, precision, kname), "kernel": kname,
+            "algorithmic_bytes_per_launch": k_amount / max(k_launch, 1),
+            "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": which,
+            "model": "16 B/node-update fp32 (32 fp64) + 4*nnz + 4*(n+1) CSR bytes per iteration (SURVEY 8d); "
+                     "achieved = that / CUDA-event time of the kernel's launches on the solver stream"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2509_18612_b200 import LCB_FP32, LCB_FP64
-    from paper_2509_18612_b200 import liftcut as lc
     from paper_2509_18612_b200.dist import Comm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -287,132 +458,58 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = Comm.from_torch(local)
-    prec = LCB_FP32 if args.precision == "fp32" else LCB_FP64
-    g, cfg, desc = workload(args.config, world, args.precision)
-    # batched search rounds measured slower on config 5 (B=256 already fills the GPU; see
-    # profiles/round1_kernel_ab.md), so the bench keeps the sequential evolve() order
-    # config 5 shards independent searches: rank r runs its own solve with seed
-    # k*N + r and no member sharding; the best cut is reduced over ranks with NCCL at the end
-    independent = args.config == "c5" and world > 1
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=None if independent else comm, batched_search=False)
-    seed_of = (lambda k: k * world + rank) if independent else (lambda k: k)
-    solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[int(cfg.algorithm)]
-    g.handle(local)  # inputs resident in HBM before timing
-
+    arm = Arm(world, rank, local, comm)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-
-    for _ in range(args.warmup):
-        solve(g, cfg, seed=0, opts=opts)
-    barrier()
-
     sampler = ClockSampler(local) if rank == 0 else None
-    l0 = lc.counters()[0]
-    dev_ms, step_ms, step_bytes, launches, ups, best = 0.0, 0.0, 0.0, 0, 0, 0
-    kst = {"k_step": [0.0, 0.0, 0.0], "k_resident": [0.0, 0.0, 0.0], "k_dense_step": [0.0, 0.0, 0.0]}
-    for k in range(args.steps):
-        flush.fill_(k & 0xFF)  # L2 flush between timed steps (untimed)
-        barrier()
-        out = solve(g, cfg, seed=seed_of(k), opts=opts)
-        dev_ms += out.solve_ms
-        step_ms += out.step_ms
-        step_bytes += out.step_bytes
-        launches += out.step_launches
-        for kname, vals in out.kernel_stats.items():
-            for i in range(3):
-                kst[kname][i] += vals[i]
-        ups += out.node_updates
-        best = max(best, out.best.cut_value)
-        if lc.cut_value(g, out.best.assignment) != out.best.cut_value:
-            raise RuntimeError("reported cut does not recompute")
-    barrier()
-    gpu_launches = lc.counters()[0] - l0
+    main = measure(arm, args.config, args.precision, args.steps, args.warmup, flush, with_e2e=True)
     clocks = sampler.stop() if sampler else None
 
-    # e2e: the public API with HOST buffers (graph upload + assignment download inside)
-    h0, d0 = lc.counters()[1:]
-    barrier()
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        gh = lc.Graph.from_csr(g.node_count(), g.offsets, g.adjacency)
-        solve(gh, cfg, seed=seed_of(k), opts=opts)
-        gh.release()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    h1, d1 = lc.counters()[1:]
-
-    t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms, max_e2e = float(t[0]), float(t[1])
-    if world > 1:  # best cut over ranks (identical on every rank unless the runs are independent)
-        bt = torch.tensor([best], dtype=torch.int64, device=f"cuda:{local}")
-        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
-        best = int(bt[0])
-    total_ups = ups * world
-    value = total_ups / (max_ms / 1e3)
-    e2e_value = total_ups / max_e2e
+    extras = []
+    if world == 1 and args.extras and args.config == DEFAULT_CONFIG:
+        plan = [("c2", "fp32", 3, 3), ("c3", "fp32", 3, 3), ("c5", "fp32", 1, 1), ("c4", "fp64", 2, 3)]
+        for name, prec, steps, warm in plan:
+            t0 = time.perf_counter()
+            try:
+                r = measure(arm, name, prec, steps, warm, flush, with_e2e=False)
+                extras.append({"config_id": name, "precision": prec, "steps": steps, "warmup": warm,
+                               "workload": WORKLOADS[name]["desc"], "value": r["value"], "unit": UNIT,
+                               "ms_per_step": r["ms_per_step"], "best_cut": r["best_cut"], "dtype": r["dtype"],
+                               "roofline_frac": r["roofline"]["frac"], "roofline": r["roofline"],
+                               "wall_s": round(time.perf_counter() - t0, 1)})
+            except Exception as e:  # noqa: BLE001
+                extras.append({"config_id": name, "precision": prec, "error": str(e)[:300]})
+            torch.cuda.empty_cache()
 
     if rank == 0:
-        peak, which = measured_peaks()
-        # roofline of the dominant step kernel (largest share of step-kernel time)
-        kname = max(kst, key=lambda k: kst[k][0])
-        k_ms, k_launch, k_amount = kst[kname]
-        shares = {k: v[0] / max(step_ms, 1e-9) for k, v in kst.items() if v[1]}
-        if kname == "k_dense_step":
-            tpeak, twhich = measured_tensor_peak()
-            achieved = k_amount / (k_ms / 1e3) / 1e12
-            roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
-                    "frac": achieved / tpeak, "traffic": ncu_traffic(args.config, args.precision, kname),
-                    "kernel": kname, "algorithmic_flops_per_launch": k_amount / max(k_launch, 1),
-                    "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": twhich,
-                    "model": "2*n^2*W algorithmic flops per iteration (SURVEY 8d). Executed MMA work differs "
-                             "per 32-node K step: bf16 hi/mid/lo planes before saturation, mid/lo skipped when "
-                             "all zero, e4m3 MMAs on corner-valued steps (DESIGN.md K3)"}
-        else:
-            achieved = k_amount / (k_ms / 1e3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": ncu_traffic(args.config, args.precision, kname),
-                    "kernel": kname, "algorithmic_bytes_per_launch": k_amount / max(k_launch, 1),
-                    "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": which,
-                    "model": "16 B/node-update fp32 (32 fp64) + CSR bytes per iteration (SURVEY 8d)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            T, reps = ref_sample(args.config)
             try:
-                u, dt, _, thr = cpu_reference_step(g, cfg, 1, T, reps)
-                cpu = {"value": u / dt, "unit": UNIT, "cores": thr, "kind": "reference",
-                       "sample": f"unmodified reference solve (oracle/_ref) of the same graph/config with "
-                                 f"T={T} instead of {cfg.ascent.iterations}"
-                                 + (f", {reps} solves" if reps > 1 else "") + f", {thr} host threads, {dt:.1f} s"}
+                rg = reference_graph(args.config)
+                T, reps = ref_sample(args.config)
+                thr = os.cpu_count() or 1
+                u, asc, sec, _ = cpu_reference_step(rg, args.config, 1, T, reps, thr)
+                cpu = {"value": u / asc, "unit": UNIT, "cores": thr, "kind": "reference",
+                       "sample": f"unmodified reference solve (oracle/_ref) of the same graph/config with T={T} "
+                                 f"instead of 500" + (f", {reps} solves" if reps > 1 else "") +
+                                 f", {thr} host threads; node-updates / StageTimes.ascent_s ({asc:.1f} s of "
+                                 f"{sec:.1f} s solve wall)"}
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+        cfgd = config_dict(args.config, world, args.precision)
+        cfgd["timing"] = "CUDA events on the solver stream around each whole solve, sum over steps, max over ranks"
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if prec == LCB_FP32 else "f64", "data": "synthetic",
-            "best_cut": best,
-            "config": {"workload": desc, "config_id": args.config, "graph_nodes": g.node_count(),
-                       "graph_edges": g.edge_count(), "members_per_gpu": cfg.batch_size,
-                       "global_batch": cfg.batch_size * world,
-                       "node_updates_per_step": total_ups // args.steps,
-                       "l2": "flushed between timed steps (512 MB write); each step is a full solve",
-                       "parallelism": f"member-sharded dp{world}" if world > 1 else "single GPU",
-                       "timing": "CUDA events on the solver stream, sum over steps, max over ranks"},
-            "roofline": roof,
-            "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": (h1 - h0) // args.steps,
-                    "d2h_bytes_per_step": (d1 - d0) // args.steps},
-            "gpu_launches": gpu_launches,
-            "clocks": clocks,
-            "cpu_baseline": cpu,
+            "metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": main["dtype"], "data": "synthetic",
+            "best_cut": main["best_cut"], "config": cfgd, "roofline": main["roofline"], "e2e": main["e2e"],
+            "gpu_launches": main["gpu_launches"], "clocks": clocks, "cpu_baseline": cpu,
+            "node_updates_per_step": main["node_updates_per_step"],
+            "graph": {"nodes": main["graph_nodes"], "edges": main["graph_edges"]},
         }
-        print(json.dumps(line))
+        if extras:
+            line["extra_configs"] = extras
+        print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
     if world > 1:
@@ -420,16 +517,31 @@ def run_b200(args):
     return 0
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", dest="extras", action="store_false")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the ranks ourselves
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

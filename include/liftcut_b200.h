@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define LCB_ABI_VERSION 1
+#define LCB_ABI_VERSION 2
 
 enum lcb_status {
     LCB_OK = 0,
@@ -43,6 +43,16 @@ typedef struct lcb_comm lcb_comm;   /* NCCL communicator over the ranks of one b
 const char* lcb_last_error(void);
 int lcb_abi_version(void);
 int lcb_device_count(int* count);
+
+/* Kernel-selection knobs (no reference counterpart; B200 tuning and tests).  Names:
+ * "resident" (K2: -1 auto, 0 never, 1 whenever it fits), "stream" (K1s streaming step:
+ * 1 on, 0 off), "signrec" (K1 saturation codes: -1 auto, 0, 1), "chunk" (K1n panels:
+ * 0 off, 1 on, -1 auto), "res_split" (K2 wave-tail split), "bank_order" / "bank_refine"
+ * (K2 fp32 neighbour order, read at graph creation), "dense" (K3 adjacency at graph
+ * creation: -1 auto, 0, 1).  Defaults come from the LCB_<NAME> environment variables.
+ * Changing a knob while a solve runs in another thread is not supported. */
+int lcb_set_option(const char* name, int64_t value);
+int lcb_get_option(const char* name, int64_t* value);
 
 /* ---- graph: replaces the CSR of liftcut::Graph (graph.hpp:21-58) ------------
  * offsets int64[n+1] / adjacency uint32[offsets[n]] exactly as Graph stores them
@@ -194,8 +204,9 @@ typedef struct lcb_run_opts { /* B200-side knobs; not part of the reference conf
     int64_t* node_updates;   /* sum over batches of n * B * l * iterations executed */
     double* step_bytes;      /* algorithmic bytes of all step launches */
     double* solve_ms;        /* CUDA-event time of the whole solve on its stream */
-    double* kernel_stats;    /* [9]: K1 HBM-streaming {ms, launches, bytes}, K2 resident {ms, launches, bytes},
-                                K3 dense tensor-core {ms, launches, algorithmic flops} */
+    double* kernel_stats;    /* [12]: K1 HBM-streaming {ms, launches, bytes}, K2 resident {ms, launches, bytes},
+                                K3 dense tensor-core {ms, launches, algorithmic flops},
+                                K1s warp-specialised streaming {ms, launches, bytes} */
     lcb_trace_fn trace_fn;   /* optional per-iteration objective trace (disables early exit) */
     void* trace_ctx;
 } lcb_run_opts;
@@ -208,6 +219,16 @@ int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t 
               lcb_batch_trace* bt, int64_t bt_cap, lcb_phase_trace* pt, int64_t pt_cap,
               lcb_search_trace* st, int64_t st_cap);
 
+/* Independent runs (run_bench's per-seed loop, bench.cpp:97-136: one solve — or
+ * solve_per_component when per_component != 0 — per seed).  With a communicator, run i is
+ * solved on rank i % nranks (no member sharding inside a run), then ONE exchange: the
+ * per-run cuts (allreduce max) and the best run's outcome and assignment (first maximum in
+ * run order) from its owner.  run_cuts [nruns] optional; best_out / assignment [n] are
+ * filled on every rank. */
+int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* seeds, int64_t nruns,
+                   int32_t per_component, const lcb_run_opts* opts, int64_t* run_cuts, int64_t* best_run,
+                   lcb_outcome* best_out, uint8_t* assignment);
+
 /* ---- multi-GPU (one process per GPU; NCCL over NVLink / NVSwitch) ------------
  * Members of every batch are sharded: rank r owns global members
  * [r*B, (r+1)*B).  Per batch one allreduce(max) of the packed (cut, ~member) key
@@ -216,6 +237,14 @@ int lcb_comm_unique_id(uint8_t id[128]);
 int lcb_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device,
                     lcb_comm** out);
 void lcb_comm_destroy(lcb_comm* c);
+/* Loopback communicator: `nranks` ranks that are threads of ONE process (on one or several
+ * GPUs); the same per-batch collectives run through device staging buffers and a host
+ * barrier (no kernel waits on another).  For testing and emulating the sharded solve on
+ * fewer GPUs than ranks.  Every rank must call the same sequence of solves. */
+typedef struct lcb_loopback lcb_loopback;
+int lcb_loopback_create(int32_t nranks, lcb_loopback** out);
+void lcb_loopback_destroy(lcb_loopback* g);
+int lcb_comm_create_loopback(lcb_loopback* group, int32_t rank, int device, lcb_comm** out);
 /* Solves keep their device workspaces in a per-(device, precision) pool for reuse;
  * this frees every pooled workspace (e.g. before a large allocation elsewhere). */
 void lcb_release_workspaces(void);

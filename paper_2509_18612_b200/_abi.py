@@ -70,6 +70,8 @@ SIGNATURES = {
     "lcb_last_error": (C.c_char_p, []),
     "lcb_abi_version": (C.c_int, []),
     "lcb_device_count": (C.c_int, [P]),
+    "lcb_set_option": (C.c_int, [C.c_char_p, i64]),
+    "lcb_get_option": (C.c_int, [C.c_char_p, P]),
     "lcb_graph_create": (C.c_int, [u32, P, P, C.c_int, C.POINTER(P)]),
     "lcb_graph_destroy": (None, [P]),
     "lcb_graph_info": (C.c_int, [P, P, P, P]),
@@ -88,6 +90,10 @@ SIGNATURES = {
     "lcb_comm_unique_id": (C.c_int, [P]),
     "lcb_comm_create": (C.c_int, [P, i32, i32, C.c_int, C.POINTER(P)]),
     "lcb_comm_destroy": (None, [P]),
+    "lcb_solve_runs": (C.c_int, [P, P, P, i64, i32, P, P, P, P, P]),
+    "lcb_loopback_create": (C.c_int, [i32, C.POINTER(P)]),
+    "lcb_loopback_destroy": (None, [P]),
+    "lcb_comm_create_loopback": (C.c_int, [P, i32, C.c_int, C.POINTER(P)]),
     "lcb_counters": (None, [P, P, P]),
     "lcb_release_workspaces": (None, []),
     "lcb_pack_key": (u64, [i64, i64]),
@@ -108,7 +114,7 @@ def lib():
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
-        if L.lcb_abi_version() != 1:
+        if L.lcb_abi_version() != 2:
             raise RuntimeError("libliftcut_b200.so ABI mismatch")
         _lib = L
     return _lib

@@ -266,9 +266,8 @@ __device__ __forceinline__ bool finish_element(const DenseArgs& a, int row, int 
     float* vp = a.V + static_cast<int64_t>(c) * a.ldx + row;
     float x = *xp;
     if (act) {
-        const float y = __fsub_rn(__fmul_rn(dg, x), ax);         // Lx    (graph.cpp:120)
-        const float v = __fadd_rn(__fmul_rn(a.mu, *vp), y);      // v     (ascent.cpp:68)
-        const float raw = __fadd_rn(x, __fmul_rn(alpha, v));     // raw   (ascent.cpp:69)
+        float v = *vp;
+        const float raw = pga_raw(x, ax, v, alpha, a.mu, dg);  // ascent.cpp:66-69
         if (!isfinite(raw))
             atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
                       (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
@@ -326,9 +325,8 @@ __device__ __forceinline__ bool finish_chunk8(const DenseArgs& a, int row, int c
         float x = xs[j];
         if (act) {
             const float ax = __uint_as_float(r[j]);
-            const float y = __fsub_rn(__fmul_rn(dg, x), ax);      // Lx    (graph.cpp:120)
-            const float v = __fadd_rn(__fmul_rn(a.mu, vs[j]), y); // v     (ascent.cpp:68)
-            const float raw = __fadd_rn(x, __fmul_rn(alpha, v));  // raw   (ascent.cpp:69)
+            float v = vs[j];
+            const float raw = pga_raw(x, ax, v, alpha, a.mu, dg);  // ascent.cpp:66-69
             if (!isfinite(raw)) {
                 const int m = (a.col_base + c) / a.l;
                 atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
@@ -675,17 +673,13 @@ void launch_dense_n(const CUtensorMap& mA, const CUtensorMap& mP, DenseArgs a, f
     constexpr int full_ring = kStages * (kATileBytes + 3 * N * kBK * 2);
     constexpr int skip_ring = kSkipStages * (kATileBytes + N * kBK * 2) + 2 * N * kBK * 2;
     constexpr int smem = (full_ring > skip_ring ? full_ring : skip_ring) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dense_step<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(k_dense_step<N>), smem, "cudaFuncSetAttribute(k_dense_step)");
     // Wave quantisation: full tiles fill whole waves of the SMs; the remaining tail tiles are
     // split along K so the tail also fills one wave, reduced in a fixed order afterwards.
-    static const int sms = [] {
-        const char* e = std::getenv("LCB_DENSE_SMS");  // test hook: pretend a smaller wave
-        return e ? std::atoi(e) : num_sms(0);
-    }();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const char* sms_env = std::getenv("LCB_DENSE_SMS");  // test hook: pretend a smaller wave
+    const int sms = sms_env ? std::atoi(sms_env) : num_sms(dev);
     const int tiles = (a.n + kBM - 1) / kBM;
     int tail = tiles % sms;
     if (tail * 2 > sms || tiles < sms || partial == nullptr) tail = 0;  // tail already fills >= half a wave

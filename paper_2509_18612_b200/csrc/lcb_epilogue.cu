@@ -328,6 +328,40 @@ void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s)
     k_unpack_bits<<<(n + 255) / 256, 256, 0, s>>>(bits, n, z);
 }
 
+// loopback exchange: out[i] = op over rows r of rows[r][i] (u32 / u64, max / min)
+template <typename U, bool MAX>
+__global__ void k_reduce_rows(const U* rows, int nrows, size_t count, U* out) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        U v = rows[i];
+        for (int r = 1; r < nrows; ++r) {
+            const U w = rows[static_cast<size_t>(r) * count + i];
+            v = MAX ? (w > v ? w : v) : (w < v ? w : v);
+        }
+        out[i] = v;
+    }
+}
+
+void launch_reduce_rows(const void* rows, int nrows, size_t count, int bytes, bool is_max, void* out, cudaStream_t s) {
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>((count + 255) / 256, 1024));
+    count_launch();
+    if (bytes == 8) {
+        if (is_max)
+            k_reduce_rows<unsigned long long, true><<<blocks, 256, 0, s>>>(static_cast<const unsigned long long*>(rows),
+                                                                            nrows, count, static_cast<unsigned long long*>(out));
+        else
+            k_reduce_rows<unsigned long long, false><<<blocks, 256, 0, s>>>(
+                static_cast<const unsigned long long*>(rows), nrows, count, static_cast<unsigned long long*>(out));
+    } else {
+        if (is_max)
+            k_reduce_rows<uint32_t, true><<<blocks, 256, 0, s>>>(static_cast<const uint32_t*>(rows), nrows, count,
+                                                                 static_cast<uint32_t*>(out));
+        else
+            k_reduce_rows<uint32_t, false><<<blocks, 256, 0, s>>>(static_cast<const uint32_t*>(rows), nrows, count,
+                                                                  static_cast<uint32_t*>(out));
+    }
+}
+
 template void launch_transpose_in<float>(const double*, float*, int, int, int64_t, cudaStream_t);
 template void launch_transpose_in<double>(const double*, double*, int, int, int64_t, cudaStream_t);
 template void launch_transpose_out<float>(const float*, double*, int, int, int64_t, cudaStream_t);

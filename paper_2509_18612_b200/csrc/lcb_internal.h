@@ -36,6 +36,24 @@ __host__ __device__ inline bool ex_continue(uint32_t b) {
     return (b & EX_BIG) || ((b & EX_NZ) && !(b & EX_NOTB));
 }
 
+#ifdef __CUDACC__
+// The element update of ascent.cpp:66-69: y = deg*x - (Ax)_v, v = mu*v + y, raw = x + alpha*v.
+// fp64: separately rounded operations, bit-identical to the reference's FMA-free scalar
+// code.  fp32: ONE fused sequence shared by every kernel (K1, K1s, K2, K1n,
+// K3), so an fp32 member's trajectory does not depend on which kernel ran it, i.e. on
+// the batch width, the rank count or the early-exit flag.
+__device__ __forceinline__ float pga_raw(float x, float ax, float& v, float alpha, float mu, float dg) {
+    const float y = __fmaf_rn(dg, x, -ax);
+    v = __fmaf_rn(mu, v, y);
+    return __fmaf_rn(alpha, v, x);
+}
+__device__ __forceinline__ double pga_raw(double x, double ax, double& v, double alpha, double mu, double dg) {
+    const double y = __dsub_rn(__dmul_rn(dg, x), ax);  // Lx   graph.cpp:120
+    v = __dadd_rn(__dmul_rn(mu, v), y);                // v    ascent.cpp:68
+    return __dadd_rn(x, __dmul_rn(alpha, v));          // raw  ascent.cpp:69
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // device graph
 // ---------------------------------------------------------------------------
@@ -157,6 +175,11 @@ template <typename T>
 void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);
 template <typename T>
 int step_span(int W);  // columns covered by one warp for this W
+// K1s (lcb_stream.cu): warp-specialised streaming step over the 512-byte column slabs
+// [slab0, slab0 + nslabs) for one iteration; saturation codes of those slabs are
+// [nslabs][n][32] bytes (< 4 GB) at sgn_in / sgn_out (sgn_ld unused)
+template <typename T>
+void launch_stream(const StepArgs<T>& a, int slab0, int nslabs, bool early_exit, cudaStream_t s);
 
 template <typename T>
 void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s);
@@ -186,6 +209,8 @@ void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* k
                            int64_t member_base, int members, uint32_t* bits, cudaStream_t s,
                            int member_offset = 0);
 void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s);
+// out[i] = max / min over the nrows rows of rows[nrows][count] (bytes = 4 or 8 per element)
+void launch_reduce_rows(const void* rows, int nrows, size_t count, int bytes, bool is_max, void* out, cudaStream_t s);
 
 // init kernels (init.cpp:20-101)
 void launch_dui(const DevGraph& g, const uint64_t* col_keys, int l, double init_scale,
@@ -209,6 +234,24 @@ struct Failure {
 void cuda_check(cudaError_t e, const char* what);  // throws Failure{LCB_CUDA}
 
 int num_sms(int device);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device),
+// thread-safe, error-checked (function attributes are per device context)
+void ensure_smem_attr(const void* kernel, int bytes, const char* what);
+
+// Kernel-selection knobs: defaults, overridden by the LCB_* environment
+// variable at first use and at run time by lcb_set_option (tests, A/B runs).
+enum Opt : int {
+    OPT_RESIDENT = 0,  // K2: -1 auto, 0 never, 1 whenever the slab fits
+    OPT_STREAM,        // K1s for the HBM-streaming step: 1 on, 0 K1
+    OPT_SIGNREC,       // K1 saturation codes: -1 auto (iterate > L2), 0 off, 1 on
+    OPT_CHUNK,         // K1n L2 panels: 0 off, 1 always, -1 auto
+    OPT_RES_SPLIT,     // K2 wave-tail split into a K=1 launch
+    OPT_BANK_ORDER,    // K2 fp32 neighbour order at graph creation: 0 CSR, 1 warp, 2 half-warp
+    OPT_BANK_REFINE,   // refinement passes of that order
+    OPT_DENSE,         // K3 adjacency at graph creation: -1 auto, 0 never, 1 always
+    OPT_COUNT
+};
+int64_t option(Opt o);
 
 // graph ingest from an edge list on the device (lcb_ingest.cu): adjacency `col` [nnz]
 // stays on the device (caller owns it), offsets come back to the host

@@ -260,9 +260,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                         m = (a.col_base + colx) / a.l;
                     }
                     if (act) {
-                        const T y = rsub(rmul(dg, x), el(acc[s], e));     // Lx  (graph.cpp:120)
-                        const T v = radd(rmul(a.mu, el(vv, e)), y);        // ascent.cpp:68
-                        const T raw = radd(x, rmul(alpha, v));             // ascent.cpp:69
+                        T v = el(vv, e);
+                        const T raw = pga_raw(x, el(acc[s], e), v, alpha, a.mu, dg);  // ascent.cpp:66-69
                         if (!isfinite(raw))                                // ascent.cpp:70-72
                             atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0), (static_cast<unsigned long long>(m) << 32) |
                                                  static_cast<unsigned>(a.it));

@@ -152,9 +152,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? LCB_NARROW_MINB : 1) k_n
         }
         if (!act) continue;
         const T x = xe[e];
-        const T y = rsub(rmul(dg, x), ae[e]);    // Lx (graph.cpp:120)
-        const T v = radd(rmul(a.mu, ve[e]), y);  // ascent.cpp:68
-        const T raw = radd(x, rmul(alpha, v));   // ascent.cpp:69
+        T v = ve[e];
+        const T raw = pga_raw(x, ae[e], v, alpha, a.mu, dg);  // ascent.cpp:66-69
         if (!isfinite(raw))
             atomicMin(a.err + (a.err_seg ? m / a.err_seg : 0),
                       (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));

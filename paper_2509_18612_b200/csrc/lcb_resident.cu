@@ -221,9 +221,8 @@ __device__ __forceinline__ void row_update(const VT& xv, const VT& acc, VT& vv, 
     for (int k = 0; k < K; ++k) {
         if (!act[k]) continue;
         const T x = comp(xv, k);
-        const T y = rsub(rmul(dg, x), comp(acc, k));   // Lx   graph.cpp:120
-        const T v = radd(rmul(mu, comp(vv, k)), y);     // v    ascent.cpp:68
-        const T raw = radd(x, rmul(alpha_k[k], v));      // raw  ascent.cpp:69
+        T v = comp(vv, k);
+        const T raw = pga_raw(x, comp(acc, k), v, alpha_k[k], mu, dg);  // ascent.cpp:66-69
         if (!isfinite(raw))                              //      ascent.cpp:70-72
             atomicMin(err[k], (static_cast<unsigned long long>(mem[k]) << 32) | static_cast<unsigned>(it));
         const T cl = raw < T(-1) ? T(-1) : (raw > T(1) ? T(1) : raw);  // ascent.cpp:73
@@ -358,7 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             act[k] = valid[k] && it < tl[k];
-            if (EE && act[k] && it > 0) act[k] = ex_continue(sflag[(it + 2) % 3][k]);
+            if (EE && act[k] && it > 0) {
+                // exit test per MEMBER (ascent.cpp:91-93): OR the bits of every column of
+                // this CTA that belongs to the same member (l = 2 with K = 2)
+                uint32_t b = sflag[(it + 2) % 3][k];
+#pragma unroll
+                for (int k2 = 0; k2 < K; ++k2)
+                    if (k2 != k && valid[k2] && mem[k2] == mem[k]) b |= sflag[(it + 2) % 3][k2];
+                act[k] = ex_continue(b);
+            }
             any |= act[k];
         }
         if (!any) break;  // uniform: shared state read after a barrier
@@ -449,12 +456,8 @@ template <typename T, int K, int RPT, bool GEN, bool EE>
 void go(const ResidentArgs& a, cudaStream_t s) {
     constexpr bool COOP = sizeof(T) == 4;
     using VT = typename Slab<T, K>::type;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_resident<T, K, RPT, GEN, EE, COOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kResidentSmemMax));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(k_resident<T, K, RPT, GEN, EE, COOP>),
+                     static_cast<int>(kResidentSmemMax), "cudaFuncSetAttribute(k_resident)");
     const size_t smem = 2 * static_cast<size_t>(a.n + 1) * sizeof(VT);
     const int ctas = ((a.c_end > 0 ? a.c_end : a.W) - a.c_base + K - 1) / K;
     count_launch();
@@ -511,10 +514,7 @@ int launch_resident(const ResidentArgs& a, int K, bool ee, int elem_bytes, cudaS
         // full wave fit one K=1 wave, they run as a K=1 launch (half the SMEM traffic
         // per CTA) instead of a mostly idle K=2 wave.  With early exit a member's columns
         // must share a CTA, so the split needs l == 1 there.
-        static const int split = [] {
-            const char* e = std::getenv("LCB_RES_SPLIT");
-            return e ? std::atoi(e) : 1;
-        }();
+        const int64_t split = option(OPT_RES_SPLIT);
         int dev = 0;
         cudaGetDevice(&dev);
         const int sms = num_sms(dev);

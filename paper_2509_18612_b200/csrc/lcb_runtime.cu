@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <type_traits>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -58,15 +59,56 @@ void cuda_check(cudaError_t e, const char* what) {
 #define CK(x) cuda_check((x), #x)
 
 int num_sms(int device) {
-    static int cache[64] = {0};
+    static std::atomic<int> cache[64];
     if (device < 0 || device >= 64) return 148;
-    if (!cache[device]) {
-        int v = 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
-            v = 148;
-        cache[device] = v;
+    int v = cache[device].load(std::memory_order_relaxed);
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+        cache[device].store(v, std::memory_order_relaxed);
     }
-    return cache[device];
+    return v;
+}
+
+struct OptDef {
+    const char* name;
+    const char* env;
+    int64_t def;
+};
+constexpr OptDef kOptDefs[OPT_COUNT] = {
+    {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", 0},         {"signrec", "LCB_SIGNREC", -1},
+    {"chunk", "LCB_CHUNK", 0},        {"res_split", "LCB_RES_SPLIT", 1},   {"bank_order", "LCB_BANK_ORDER", 2},
+    {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1},
+};
+std::atomic<int64_t> g_opts[OPT_COUNT];
+std::once_flag g_opts_once;
+void init_opts() {
+    std::call_once(g_opts_once, [] {
+        for (int i = 0; i < OPT_COUNT; ++i) {
+            const char* e = std::getenv(kOptDefs[i].env);
+            g_opts[i].store(e ? std::atoll(e) : kOptDefs[i].def);
+        }
+    });
+}
+int64_t option(Opt o) {
+    init_opts();
+    return g_opts[o].load(std::memory_order_relaxed);
+}
+int opt_index(const char* name) {
+    for (int i = 0; i < OPT_COUNT; ++i)
+        if (name && std::strcmp(name, kOptDefs[i].name) == 0) return i;
+    return -1;
+}
+
+void ensure_smem_attr(const void* kernel, int bytes, const char* what) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& d : done)
+        if (d.first == kernel && d.second == dev) return;
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), what);
+    done.emplace_back(kernel, dev);
 }
 
 template <class F>
@@ -337,7 +379,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
 
     DeviceScope ds(device);
     CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));
-    if (!dev_col) CK(cudaMalloc(&g.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    if (!dev_col) CK(cudaMalloc(&g.col, sizeof(int) * (nnz + 4)));  // K1s copies aligned 16-byte runs
     CK(cudaMalloc(&g.deg64, sizeof(double) * n));
     CK(cudaMalloc(&g.deg32, sizeof(float) * n));
     CK(cudaMalloc(&g.order, sizeof(int) * n));
@@ -361,8 +403,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     g.res_perm = g.order;
     {
         // dense tensor-core path: graphs with >= 5% density (config 3), when A fits comfortably
-        const char* e = std::getenv("LCB_DENSE");
-        const int mode = e ? std::atoi(e) : -1;
+        const int mode = static_cast<int>(option(OPT_DENSE));
         const double density = n > 1 ? static_cast<double>(nnz) / (static_cast<double>(n) * (n - 1)) : 0.0;
         size_t freeb = 0, totalb = 0;
         cudaMemGetInfo(&freeb, &totalb);
@@ -423,10 +464,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             // LCB_BANK_ORDER: 0 CSR order, 1 balance the whole warp's 32 gathers over the 16
             // bank pairs, 2 (default) balance each half-warp (rows 0-15 / 16-31 of the group:
             // an 8-byte LDS is served per half-warp, 16 lanes x 8 B = one 128-byte wavefront).
-            static const int bank_order = [] {
-                const char* e = std::getenv("LCB_BANK_ORDER");
-                return e ? std::atoi(e) : 2;
-            }();
+            const int bank_order = static_cast<int>(option(OPT_BANK_ORDER));
             std::vector<uint16_t> fast;
             if (bank_order) {
                 fast = rcol;
@@ -477,10 +515,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
                     }
                 }
             }
-            static const int refine_passes = [] {  // LCB_BANK_REFINE = max passes, 0 disables
-                const char* e = std::getenv("LCB_BANK_REFINE");
-                return e ? std::max(0, std::atoi(e)) : 2;
-            }();
+            const int refine_passes = static_cast<int>(std::max<int64_t>(0, option(OPT_BANK_REFINE)));  // 0 disables
             if (!fast.empty() && refine_passes > 0 && bank_order == 2)
                 refine_bank_order(fast, rrp, static_cast<uint32_t>(H), n, refine_passes);
             CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * info.size()));
@@ -551,12 +586,105 @@ void nccl_check(ncclResult_t r, const char* what) {
 struct lcb_graph {
     lcb::DevGraph g;
 };
+namespace lcb {
+// In-process exchange between ranks that are threads of one process (one GPU or several):
+// the per-batch collectives of the solver (key / winner bits / error slots) go through
+// device staging buffers and a host barrier; kernels never wait on one another.  The
+// test / emulation backend of the multi-rank path on fewer GPUs than ranks.
+struct LoopGroup {
+    int nranks = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t gen = 0;
+    std::vector<void*> slot;  // rank r's contribution, on rank r's device
+    std::vector<size_t> cap;
+    std::vector<int> dev;
+    explicit LoopGroup(int n) : nranks(n), slot(static_cast<size_t>(n), nullptr), cap(static_cast<size_t>(n), 0),
+                                dev(static_cast<size_t>(n), 0) {}
+    ~LoopGroup() {
+        for (int r = 0; r < nranks; ++r)
+            if (slot[static_cast<size_t>(r)]) {
+                cudaSetDevice(dev[static_cast<size_t>(r)]);
+                cudaFree(slot[static_cast<size_t>(r)]);
+            }
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const int64_t g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+}  // namespace lcb
+
+struct lcb_loopback {
+    lcb::LoopGroup g;
+    explicit lcb_loopback(int n) : g(n) {}
+};
+
 struct lcb_comm {
     ncclComm_t comm = nullptr;
+    lcb::LoopGroup* loop = nullptr;
     int nranks = 1;
     int rank = 0;
     int device = 0;
+    void* gather = nullptr;  // loopback: local copies of every rank's contribution
+    size_t gather_cap = 0;
+    ~lcb_comm() {
+        if (gather) {
+            cudaSetDevice(device);
+            cudaFree(gather);
+        }
+    }
 };
+
+namespace lcb {
+bool comm_active(const lcb_comm* c) { return c && (c->comm || c->loop); }
+
+// In-place allreduce of `count` u32 / u64 words on the solver stream.
+void comm_allreduce(lcb_comm* c, void* buf, size_t count, int bytes, bool is_max, cudaStream_t st, const char* what) {
+    if (!comm_active(c) || count == 0) return;
+    if (c->comm) {
+        nccl_check(nccl().AllReduce(buf, buf, count, bytes == 8 ? ncclUint64 : ncclUint32, is_max ? ncclMax : ncclMin,
+                                    c->comm, st),
+                   what);
+        return;
+    }
+    LoopGroup& g = *c->loop;
+    const size_t nb = count * static_cast<size_t>(bytes);
+    const size_t r = static_cast<size_t>(c->rank);
+    if (g.cap[r] < nb) {  // only rank r touches its slot outside the barriers
+        if (g.slot[r]) cudaFree(g.slot[r]);
+        g.slot[r] = nullptr;
+        g.cap[r] = 0;
+        CK(cudaMalloc(&g.slot[r], nb));
+        g.cap[r] = nb;
+        g.dev[r] = c->device;
+    }
+    CK(cudaMemcpyAsync(g.slot[r], buf, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    g.barrier();
+    if (c->gather_cap < nb * static_cast<size_t>(g.nranks)) {
+        if (c->gather) cudaFree(c->gather);
+        c->gather = nullptr;
+        c->gather_cap = 0;
+        CK(cudaMalloc(&c->gather, nb * static_cast<size_t>(g.nranks)));
+        c->gather_cap = nb * static_cast<size_t>(g.nranks);
+    }
+    for (int q = 0; q < g.nranks; ++q)
+        CK(cudaMemcpyPeerAsync(static_cast<char*>(c->gather) + nb * static_cast<size_t>(q), c->device,
+                               g.slot[static_cast<size_t>(q)], g.dev[static_cast<size_t>(q)], nb, st));
+    launch_reduce_rows(c->gather, g.nranks, count, bytes, is_max, buf, st);
+    CK(cudaStreamSynchronize(st));
+    g.barrier();  // every rank has read every slot before any slot is rewritten
+}
+}  // namespace lcb
 
 namespace lcb {
 
@@ -593,7 +721,7 @@ struct Work {
     double step_bytes = 0.0;
     int64_t node_updates = 0;
     int64_t resident_iters = 0;  // iterations executed by the member-resident kernel
-    double kstats[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // K1 / K2 {ms, launches, bytes}, K3 {ms, launches, flops}
+    double kstats[12] = {0};  // K1 / K2 {ms, launches, bytes}, K3 {ms, launches, flops}, K1s {ms, launches, bytes}
 
     explicit Work(int dev) : device(dev) {
         CK(cudaSetDevice(dev));
@@ -677,10 +805,7 @@ struct PooledWork {
 // kernel wins when the on-chip slab covers the graph and the batch is wide enough to
 // fill several waves (W >= 1024 columns at K=2, any W for fp64 / small graphs).
 bool resident_preferred(const DevGraph& g, int W, size_t elem) {
-    static const int mode = [] {
-        const char* e = std::getenv("LCB_RESIDENT");
-        return e ? std::atoi(e) : -1;  // -1 auto, 0 never, 1 always (when it fits)
-    }();
+    const int64_t mode = option(OPT_RESIDENT);  // -1 auto, 0 never, 1 always (when it fits)
     if (mode == 0) return false;
     if (mode == 1) return true;
     if (elem == 8) return true;
@@ -833,13 +958,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
             return static_cast<int64_t>(v > 0 ? v : (126 << 20));
         }();
-        static const int chunk_mode = [] {
-            const char* e = std::getenv("LCB_CHUNK");
-            // 0 never (default), 1 always, -1 auto (iterate > 2 x L2 and the panel pair fits).
-            // Off by default: on config 4 (ER 1M, W=512) the panel kernel is latency-bound at
-            // 5.5 ms/iteration vs 4.46 ms for K1 (profiles/round1_narrow.md).
-            return e ? std::atoi(e) : 0;
-        }();
+        // 0 never (default), 1 always, -1 auto (iterate > 2 x L2 and the panel pair fits).
+        // Off by default: on config 4 (ER 1M, W=512) the panel kernel is latency-bound at
+        // 5.5 ms/iteration vs 4.46 ms for K1 (profiles/round1_narrow.md).
+        const int64_t chunk_mode = option(OPT_CHUNK);
         const int P = narrow_panel_cols(static_cast<int>(sizeof(T)));
         const int64_t panel = static_cast<int64_t>(g.n) * W * static_cast<int64_t>(sizeof(T));
         const int64_t narrow = static_cast<int64_t>(g.n) * P * static_cast<int64_t>(sizeof(T));
@@ -895,10 +1017,17 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     // dependent code load makes K1 slower (config 5: 169.6 -> 172.8 us, config 2 W=1024:
     // 51.2 -> 62.0 us; profiles/round1_kernel_ab.md).  LCB_SIGNREC=0 never, 1 always,
     // default: iterate buffer larger than L2.
-    static const int signrec = [] {
-        const char* e = std::getenv("LCB_SIGNREC");
-        return e ? std::atoi(e) : -1;
-    }();
+    const int64_t signrec = option(OPT_SIGNREC);
+    // K1s (lcb_stream.cu), the warp-specialised streaming step: LCB_STREAM=0 keeps K1
+    const int64_t stream_mode = option(OPT_STREAM);
+    const int sspan = 32 * static_cast<int>(16 / sizeof(T));  // one 512-byte slab
+    const int nslabs = (W + sspan - 1) / sspan;
+    // slab-outer order (all iterations of one slab before the next: members are independent,
+    // ascent.cpp:52, so the slab's codes stay L2-resident across iterations) unless early exit
+    // needs every column of a member in the same launch
+    const bool slab_outer = !ee || sspan % l == 0;
+    const bool use_stream = stream_mode != 0 && !trace_host && step_span<T>(W) == sspan && w.ld % sspan == 0 &&
+                            static_cast<int64_t>(g.n) * 32 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
     static const int64_t l2_bytes = [] {
         int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
@@ -906,13 +1035,93 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     }();
     uint8_t* codes[2] = {nullptr, nullptr};
     const int span = step_span<T>(W);
-    const bool codes_on = signrec == 1 || (signrec != 0 && static_cast<int64_t>(g.n) * w.ld *
-                                                                   static_cast<int64_t>(sizeof(T)) > l2_bytes);
+    const bool codes_on = use_stream || signrec == 1 ||
+                          (signrec != 0 && static_cast<int64_t>(g.n) * w.ld * static_cast<int64_t>(sizeof(T)) > l2_bytes);
     if (codes_on && span == 32 * static_cast<int>(16 / sizeof(T)) && w.ld % span == 0) {
+        // K1: [n][sgn_ld] interleaved; K1s: [slabs][n][32] (one slab when slab-outer)
         a.sgn_ld = (w.ld / span) * 32;
-        const size_t bytes = static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld);
+        const size_t bytes = use_stream ? static_cast<size_t>(g.n) * 32 * (slab_outer ? 1 : nslabs)
+                                        : static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld);
         codes[0] = w.sgn.ensure(2 * bytes);
         codes[1] = codes[0] + bytes;
+    }
+    if (use_stream && slab_outer) {
+        // ---- K1s, slab-outer: for each 512-byte column slab, all its iterations
+        CK(cudaEventRecord(w.ev0, w.st));
+        std::vector<int64_t> slab_it(static_cast<size_t>(nslabs), 0);
+        double updates = 0.0;
+        int64_t launches = 0, it_max = 0;
+        for (int sl = 0; sl < nslabs; ++sl) {
+            const int c_lo = sl * sspan, c_hi = std::min(W, c_lo + sspan);
+            int64_t ts = iters;
+            if (seg_iters && err_seg > 0) {  // longest candidate among the slab's segments
+                ts = 0;
+                for (int c = c_lo; c < c_hi; c += err_seg * l)
+                    ts = std::max(ts, (*seg_iters)[static_cast<size_t>(c / (err_seg * l))]);
+                ts = std::max(ts, (*seg_iters)[static_cast<size_t>((c_hi - 1) / (err_seg * l))]);
+            }
+            const int m_lo = c_lo / l, m_hi = (c_hi - 1) / l + 1;  // members touching the slab
+            if (ee) CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * 3 * members, w.st));
+            int64_t t = 0;
+            for (; t < ts; ++t) {
+                a.x_in = w.X[t & 1].p;
+                a.x_out = w.X[(t + 1) & 1].p;
+                a.it = static_cast<int>(t);
+                a.sgn_in = t > 0 ? codes[t & 1] : nullptr;
+                a.sgn_out = codes[(t + 1) & 1];
+                if (ee) {
+                    a.flags_prev = F + ((t + 2) % 3) * members;
+                    a.flags_cur = F + (t % 3) * members;
+                    a.flags_zero = F + ((t + 1) % 3) * members;
+                }
+                launch_stream<T>(a, sl, 1, ee, w.st);
+                ++launches;
+                if (ee && ((t + 1) % 32 == 0) && t + 1 < ts) {  // stop once the slab's members left
+                    uint32_t* hf = w.host_flags(members);
+                    d2h(hf, a.flags_cur, sizeof(uint32_t) * members, w.st);
+                    CK(cudaStreamSynchronize(w.st));
+                    bool any = false;
+                    for (int m = m_lo; m < m_hi && !any; ++m) any = ex_continue(hf[m]);
+                    if (!any && !tlim_arr) {
+                        ++t;
+                        break;
+                    }
+                }
+            }
+            slab_it[static_cast<size_t>(sl)] = t;
+            it_max = std::max(it_max, t);
+            updates += static_cast<double>(t) * g.n * (c_hi - c_lo);
+        }
+        // every slab's result into X[it_max & 1]
+        for (int sl = 0; sl < nslabs; ++sl) {
+            const int64_t t = slab_it[static_cast<size_t>(sl)];
+            if ((t ^ it_max) & 1) {
+                const size_t pitch = sizeof(T) * static_cast<size_t>(w.ld);
+                CK(cudaMemcpy2DAsync(w.X[it_max & 1].p + static_cast<size_t>(sl) * sspan, pitch,
+                                     w.X[t & 1].p + static_cast<size_t>(sl) * sspan, pitch, sizeof(T) * sspan,
+                                     static_cast<size_t>(g.n), cudaMemcpyDeviceToDevice, w.st));
+            }
+        }
+        CK(cudaEventRecord(w.ev1, w.st));
+        CK(cudaGetLastError());
+        d2h(w.h_keys, a.err, sizeof(unsigned long long) * err_slots, w.st);
+        CK(cudaStreamSynchronize(w.st));
+        r.err = w.h_keys[0];
+        r.errs.assign(w.h_keys, w.h_keys + err_slots);
+        r.iters = it_max;
+        r.final_buf = static_cast<int>(it_max & 1);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+        w.step_ms += ms;
+        w.step_launches += launches;
+        const double bytes = 4.0 * sizeof(T) * updates +
+                             static_cast<double>(launches) / std::max(1, nslabs) * (4.0 * g.nnz + 4.0 * (g.n + 1));
+        w.step_bytes += bytes;
+        w.kstats[9] += ms;
+        w.kstats[10] += static_cast<double>(launches);
+        w.kstats[11] += bytes;
+        w.node_updates += static_cast<int64_t>(updates);
+        return r;
     }
     CK(cudaEventRecord(w.ev0, w.st));
     int64_t it = 0;
@@ -933,7 +1142,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             a.flags_cur = F + (it % 3) * members;
             a.flags_zero = F + ((it + 1) % 3) * members;
         }
-        launch_step<T>(a, ee, MODE_STEP, w.st);
+        if (use_stream)
+            launch_stream<T>(a, 0, (a.W + sspan - 1) / sspan, ee, w.st);
+        else
+            launch_step<T>(a, ee, MODE_STEP, w.st);
         if (trace_host) {
             // objective after the step: x'Lx per member (ascent.cpp:78-88)
             StepArgs<T> b = a;
@@ -987,9 +1199,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     const double bytes = static_cast<double>(it) *
                          (4.0 * sizeof(T) * static_cast<double>(g.n) * W + 4.0 * g.nnz + 4.0 * (g.n + 1));
     w.step_bytes += bytes;
-    w.kstats[0] += ms;
-    w.kstats[1] += static_cast<double>(it);
-    w.kstats[2] += bytes;
+    const int ks = use_stream ? 9 : 0;
+    w.kstats[ks] += ms;
+    w.kstats[ks + 1] += static_cast<double>(it);
+    w.kstats[ks + 2] += bytes;
     w.node_updates += it * static_cast<int64_t>(g.n) * W;
     return r;
 }
@@ -1067,9 +1280,9 @@ struct Solver {
     // With several ranks a non-finite value on one rank must stop every rank the same
     // way (the collectives that follow must match): min-reduce the error slots.
     void sync_errors(IterResult& ir) {
-        if (!(comm && comm->comm)) return;
+        if (!comm_active(comm)) return;
         const size_t slots = ir.errs.size();
-        nccl_check(nccl().AllReduce(w.err.p, w.err.p, slots, ncclUint64, ncclMin, comm->comm, w.st), "allreduce(err)");
+        comm_allreduce(comm, w.err.p, slots, 8, false, w.st, "allreduce(err)");
         d2h(w.h_keys, w.err.p, sizeof(unsigned long long) * slots, w.st);
         CK(cudaStreamSynchronize(w.st));
         ir.errs.assign(w.h_keys, w.h_keys + slots);
@@ -1181,13 +1394,9 @@ struct Solver {
         launch_cut_count(g, Z, words, cuts, w.st);
         unsigned long long* key = w.keys.ensure(8);
         launch_argmax(cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
-        if (comm && comm->comm)
-            nccl_check(nccl().AllReduce(key, key, 1, ncclUint64, ncclMax, comm->comm, w.st), "allreduce(key)");
+        comm_allreduce(comm, key, 1, 8, true, w.st, "allreduce(key)");
         launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
-        if (comm && comm->comm)
-            nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
-                                        comm->comm, w.st),
-                       "allreduce(winner)");
+        comm_allreduce(comm, w.win.p, static_cast<size_t>(words_n), 4, true, w.st, "allreduce(winner)");
         d2h(w.h_keys, key, sizeof(unsigned long long), w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
@@ -1261,10 +1470,7 @@ struct Solver {
         launch_cut_count(g, out.Z, words, cuts, w.st);
         out.d_keys = w.keys.ensure(static_cast<size_t>(std::max(K, 8)));
         launch_argmax(cuts, members, static_cast<int>(B), member_base, out.d_keys, w.st);
-        if (comm && comm->comm)
-            nccl_check(nccl().AllReduce(out.d_keys, out.d_keys, static_cast<size_t>(K), ncclUint64, ncclMax,
-                                        comm->comm, w.st),
-                       "allreduce(keys)");
+        comm_allreduce(comm, out.d_keys, static_cast<size_t>(K), 8, true, w.st, "allreduce(keys)");
         d2h(w.h_keys, out.d_keys, sizeof(unsigned long long) * K, w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
@@ -1288,10 +1494,7 @@ struct Solver {
         const int sgi = m.seg_of[static_cast<size_t>(k)];
         launch_extract_winner(m.Z, g.n, m.d_keys + sgi, member_base, static_cast<int>(B) * (sgi + 1), w.win.p, w.st,
                               static_cast<int>(B) * sgi);
-        if (comm && comm->comm)
-            nccl_check(nccl().AllReduce(w.win.p, w.win.p, static_cast<size_t>(words_n), ncclUint32, ncclMax,
-                                        comm->comm, w.st),
-                       "allreduce(winner)");
+        comm_allreduce(comm, w.win.p, static_cast<size_t>(words_n), 4, true, w.st, "allreduce(winner)");
     }
 
     // note_batch — solver.cpp:145-150 (winner bits are in w.win)
@@ -1675,8 +1878,8 @@ void solve_top(const DevGraph& g, const lcb_config& cfg, uint64_t seed, int per_
         finish();
         return;
     }
-    if (o.comm && o.comm->nranks > 1)
-        fail(LCB_VALIDATION, "multi-GPU solve of a disconnected graph: shard per component instead");
+    // multi-rank: every rank walks the same components in the same order (the graph is
+    // replicated) and each component solve is member-sharded with its own collectives
     std::memset(assignment, 0, static_cast<size_t>(g.n));
     out.batch_index = -1;
     out.member_index = -1;
@@ -1817,6 +2020,23 @@ extern "C" {
 
 const char* lcb_last_error(void) { return g_last_error.c_str(); }
 int lcb_abi_version(void) { return LCB_ABI_VERSION; }
+
+int lcb_set_option(const char* name, int64_t value) {
+    return guard([&] {
+        const int i = opt_index(name);
+        if (i < 0) fail(LCB_VALIDATION, std::string("unknown option '") + (name ? name : "") + "'");
+        init_opts();
+        g_opts[i].store(value);
+    });
+}
+
+int lcb_get_option(const char* name, int64_t* value) {
+    return guard([&] {
+        const int i = opt_index(name);
+        if (i < 0 || !value) fail(LCB_VALIDATION, std::string("unknown option '") + (name ? name : "") + "'");
+        *value = option(static_cast<Opt>(i));
+    });
+}
 
 int lcb_device_count(int* count) {
     return guard([&] { CK(cudaGetDeviceCount(count)); });
@@ -2123,6 +2343,107 @@ int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t 
             solve_top<float>(g->g, *cfg, seed, per_component, o, *out, assignment, sinks);
         else
             solve_top<double>(g->g, *cfg, seed, per_component, o, *out, assignment, sinks);
+    });
+}
+
+int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* seeds, int64_t nruns,
+                   int32_t per_component, const lcb_run_opts* opts, int64_t* run_cuts, int64_t* best_run,
+                   lcb_outcome* best_out, uint8_t* assignment) {
+    return guard([&] {
+        if (!g || !cfg || !seeds || !best_out || !assignment) fail(LCB_VALIDATION, "null argument");
+        if (nruns < 1) fail(LCB_VALIDATION, "solve_runs: need at least one run");
+        validate_config(*cfg);
+        lcb_run_opts o{};
+        o.precision = LCB_FP64;
+        o.host_init = -1;
+        if (opts) o = *opts;
+        lcb_comm* comm = o.comm;
+        o.comm = nullptr;  // runs are independent: each is solved on one rank (bench.cpp:97-136)
+        const int nr = comm ? comm->nranks : 1, rk = comm ? comm->rank : 0;
+        const DevGraph& G = g->g;
+        DeviceScope ds(G.device);
+        const int words = (G.n + 31) / 32;
+        std::vector<unsigned long long> enc(static_cast<size_t>(nruns), 0ull);  // cut + 1 where owned
+        std::vector<uint8_t> z(static_cast<size_t>(G.n)), zbest(static_cast<size_t>(G.n), 0);
+        lcb_outcome local_best{};
+        int64_t local_run = -1, local_cut = -1;
+        for (int64_t i = rk; i < nruns; i += nr) {
+            lcb_outcome out{};
+            TraceSinks sinks{nullptr, 0, nullptr, 0, nullptr, 0};
+            if (o.precision == LCB_FP32)
+                solve_top<float>(G, *cfg, seeds[i], per_component, o, out, z.data(), sinks);
+            else
+                solve_top<double>(G, *cfg, seeds[i], per_component, o, out, z.data(), sinks);
+            enc[static_cast<size_t>(i)] = static_cast<unsigned long long>(out.cut_value) + 1ull;
+            if (out.cut_value > local_cut) {
+                local_cut = out.cut_value;
+                local_run = i;
+                local_best = out;
+                zbest = z;
+            }
+        }
+        // one exchange: per-run cuts, then the winner's outcome and assignment (zeros elsewhere)
+        const size_t ow = (sizeof(lcb_outcome) + 7) / 8;
+        const size_t total = static_cast<size_t>(nruns) + ow + 2 * static_cast<size_t>(words);
+        unsigned long long* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(unsigned long long) * total));
+        struct Free {
+            void* p;
+            ~Free() { cudaFree(p); }
+        } fr{d};
+        cudaStream_t st = nullptr;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct SFree {
+            cudaStream_t s;
+            ~SFree() { cudaStreamDestroy(s); }
+        } sf{st};
+        h2d(d, enc.data(), sizeof(unsigned long long) * enc.size(), st);
+        comm_allreduce(comm, d, static_cast<size_t>(nruns), 8, true, st, "allreduce(run cuts)");
+        d2h(enc.data(), d, sizeof(unsigned long long) * enc.size(), st);
+        CK(cudaStreamSynchronize(st));
+        int64_t win = 0;
+        for (int64_t i = 1; i < nruns; ++i)
+            if (enc[static_cast<size_t>(i)] > enc[static_cast<size_t>(win)]) win = i;  // first maximum
+        std::vector<unsigned long long> pay(ow + 2 * static_cast<size_t>(words), 0ull);
+        if (win % nr == rk) {
+            std::memcpy(pay.data(), &local_best, sizeof(lcb_outcome));
+            uint32_t* bits = reinterpret_cast<uint32_t*>(pay.data() + ow);
+            for (int v = 0; v < G.n; ++v)
+                if (zbest[static_cast<size_t>(v)]) bits[v >> 5] |= 1u << (v & 31);
+            if (local_run != win) fail(LCB_ERROR, "solve_runs: winner bookkeeping");
+        }
+        h2d(d + nruns, pay.data(), sizeof(unsigned long long) * pay.size(), st);
+        comm_allreduce(comm, d + nruns, pay.size(), 8, true, st, "allreduce(winner)");
+        d2h(pay.data(), d + nruns, sizeof(unsigned long long) * pay.size(), st);
+        CK(cudaStreamSynchronize(st));
+        std::memcpy(best_out, pay.data(), sizeof(lcb_outcome));
+        const uint32_t* bits = reinterpret_cast<const uint32_t*>(pay.data() + ow);
+        for (int v = 0; v < G.n; ++v) assignment[v] = static_cast<uint8_t>((bits[v >> 5] >> (v & 31)) & 1u);
+        if (run_cuts)
+            for (int64_t i = 0; i < nruns; ++i) run_cuts[i] = static_cast<int64_t>(enc[static_cast<size_t>(i)]) - 1;
+        if (best_run) *best_run = win;
+    });
+}
+
+int lcb_loopback_create(int32_t nranks, lcb_loopback** out) {
+    return guard([&] {
+        if (nranks < 1 || !out) fail(LCB_VALIDATION, "bad nranks");
+        *out = new lcb_loopback(nranks);
+    });
+}
+
+void lcb_loopback_destroy(lcb_loopback* g) { delete g; }
+
+int lcb_comm_create_loopback(lcb_loopback* group, int32_t rank, int device, lcb_comm** out) {
+    return guard([&] {
+        if (!group || !out) fail(LCB_VALIDATION, "null argument");
+        if (rank < 0 || rank >= group->g.nranks) fail(LCB_VALIDATION, "bad rank / nranks");
+        auto c = std::make_unique<lcb_comm>();
+        c->loop = &group->g;
+        c->nranks = group->g.nranks;
+        c->rank = rank;
+        c->device = device;
+        *out = c.release();
     });
 }
 

@@ -66,7 +66,36 @@ class Comm:
         dist.broadcast_object_list(obj, src=0)
         return cls(world, rank, device, obj[0])
 
+    @classmethod
+    def loopback(cls, group: "LoopbackGroup", rank: int, device: int = 0) -> "Comm":
+        """Rank `rank` of an in-process loopback group (lcb_comm_create_loopback)."""
+        c = cls.__new__(cls)
+        c.nranks, c.rank, c.device = group.nranks, rank, device
+        h = C.c_void_p()
+        if _abi.lib().lcb_comm_create_loopback(group.handle, rank, device, C.byref(h)) != 0:
+            raise RuntimeError(f"lcb_comm_create_loopback: {_abi.last_error()}")
+        c.handle = h
+        return c
+
     def close(self):
         if self.handle:
             _abi.lib().lcb_comm_destroy(self.handle)
+            self.handle = None
+
+
+class LoopbackGroup:
+    """`nranks` ranks that are threads of this process (lcb_loopback_create): the solver's
+    per-batch collectives run through device staging buffers and a host barrier.  Used to
+    run the member-sharded solve on fewer GPUs than ranks (tests)."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        h = C.c_void_p()
+        if _abi.lib().lcb_loopback_create(nranks, C.byref(h)) != 0:
+            raise RuntimeError(f"lcb_loopback_create: {_abi.last_error()}")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _abi.lib().lcb_loopback_destroy(self.handle)
             self.handle = None

@@ -396,6 +396,18 @@ def write_graph_file(g: Graph, path: str):
 
 def generate_er(n: int, p: float, seed: int) -> Graph:
     """ER G(n, p) with the reference's pair stream (graph.cpp:200-213), vectorised."""
+    u, v = generate_er_edges(n, p, seed)
+    return Graph(n, np.stack([u, v], 1))
+
+
+def generate_er_device(n: int, p: float, seed: int, device: Optional[int] = None) -> Graph:
+    """generate_er with the CSR built on the GPU (lcb_graph_from_edges)."""
+    u, v = generate_er_edges(n, p, seed)
+    return Graph.from_edges_device(n, np.stack([u, v], 1), device)
+
+
+def generate_er_edges(n: int, p: float, seed: int):
+    """The edge stream of generate_er (graph.cpp:200-213): pairs u < v in row order."""
     if n < 1:
         raise ValidationError("generate_er: n must be >= 1")
     if not (0.0 <= p <= 1.0):
@@ -419,8 +431,8 @@ def generate_er(n: int, p: float, seed: int) -> Graph:
         vs.append(u + 1 + hit.astype(np.int64))
         base += cnt
     if not us:
-        return Graph(n, np.zeros((0, 2), dtype=np.int64))
-    return Graph(n, np.stack([np.concatenate(us), np.concatenate(vs)], 1))
+        return np.zeros(0, dtype=np.int64), np.zeros(0, dtype=np.int64)
+    return np.concatenate(us), np.concatenate(vs)
 
 
 # ---------------------------------------------------------------------------
@@ -832,7 +844,7 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
     z = np.zeros(g.node_count(), dtype=np.uint8)
     bt, pt, st = (_abi.BatchTrace * cap)(), (_abi.PhaseTrace * cap)(), (_abi.SearchTrace * cap)()
     step_ms, step_bytes, solve_ms = C.c_double(0), C.c_double(0), C.c_double(0)
-    kst = (C.c_double * 9)()
+    kst = (C.c_double * 12)()
     launches, nupd = C.c_int64(0), C.c_int64(0)
     ro = _abi.RunOpts(precision=default_precision() if opts.precision is None else opts.precision,
                       host_init=opts.host_init, batched_search=int(opts.batched_search),
@@ -864,7 +876,75 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
         batches_run=out.batches_run, step_ms=step_ms.value, step_launches=launches.value,
         node_updates=nupd.value, step_bytes=step_bytes.value, solve_ms=solve_ms.value,
         kernel_stats={"k_step": tuple(kst[0:3]), "k_resident": tuple(kst[3:6]),
-                      "k_dense_step": tuple(kst[6:9])})
+                      "k_dense_step": tuple(kst[6:9]), "k_stream": tuple(kst[9:12])})
+
+
+@dataclass
+class RunsOutcome:
+    """solve_runs: every run's best cut and the best run (first maximum in run order)."""
+    run_cuts: np.ndarray
+    best_run: int
+    best: CutSolution
+    stage_times: StageTimes
+    batches_run: int
+
+
+def solve_runs(g: Graph, cfg: SolverConfig, seeds, per_component: bool = True,
+               opts: Optional[RunOptions] = None) -> RunsOutcome:
+    """Independent runs, one per seed (run_bench's loop, bench.cpp:97-136): run i is solved
+    on rank i % nranks of ``opts.comm`` (or locally), then one exchange of the per-run cuts
+    and the best run's assignment (lcb_solve_runs)."""
+    cfg.validate()
+    opts = opts or RunOptions()
+    seeds = np.ascontiguousarray([int(s) & _M64 for s in seeds], dtype=np.uint64)
+    c = cfg.to_abi()
+    ro = _abi.RunOpts(precision=default_precision() if opts.precision is None else opts.precision,
+                      host_init=opts.host_init, batched_search=int(opts.batched_search),
+                      comm=opts.comm.handle if opts.comm is not None else None)
+    cuts = np.zeros(len(seeds), dtype=np.int64)
+    best_run = C.c_int64(-1)
+    out = _abi.Outcome()
+    z = np.zeros(g.node_count(), dtype=np.uint8)
+    dev = opts.comm.device if opts.comm is not None else None
+    _check(_abi.lib().lcb_solve_runs(g.handle(dev), C.byref(c), _ptr(seeds), len(seeds), int(per_component),
+                                     C.byref(ro), _ptr(cuts), C.byref(best_run), C.byref(out), _ptr(z)))
+    b = best_run.value
+    return RunsOutcome(cuts, b, CutSolution(z, out.cut_value, algorithm_to_string(Algorithm(cfg.algorithm)),
+                                            int(seeds[b]), out.batch_index, out.member_index, out.wall_s),
+                       StageTimes(out.init_s, out.ascent_s, out.rounding_s, out.search_s), out.batches_run)
+
+
+def set_option(name: str, value: int) -> None:
+    """Kernel-selection knob of the library (lcb_set_option): resident, stream, signrec,
+    chunk, res_split, bank_order, bank_refine, dense."""
+    _check(_abi.lib().lcb_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64()
+    _check(_abi.lib().lcb_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: set knobs for the duration of a block, restore them after.
+
+        with lc.options(resident=0, stream=1): ...
+    """
+
+    def __init__(self, **kw):
+        self.kw, self.old = kw, {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
+        return False
 
 
 def counters():

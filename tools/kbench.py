@@ -10,7 +10,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import ba_graph, er_sparse  # noqa: E402
+import numpy as np  # noqa: E402
+
+from bench import ba_edges, fast_gnp_edges  # noqa: E402
 from paper_2509_18612_b200 import LCB_FP32, LCB_FP64  # noqa: E402
 from paper_2509_18612_b200 import liftcut as lc  # noqa: E402
 
@@ -23,7 +25,8 @@ ap.add_argument("--tag", default="")
 ap.add_argument("--graph", default="ba", choices=["ba", "er"])
 ap.add_argument("--quco-only", action="store_true")
 a = ap.parse_args()
-g = ba_graph(a.n, 4, 0) if a.graph == "ba" else er_sparse(a.n, 10.0, 0)
+u, v = ba_edges(a.n, 4, 0) if a.graph == "ba" else fast_gnp_edges(a.n, 10.0 / (a.n - 1), 0)
+g = lc.Graph.from_edges_device(a.n, np.stack([u, v], 1))
 prec = LCB_FP32 if a.precision == "fp32" else LCB_FP64
 for algo, l in ((lc.Algorithm.pQUCO, 1), (lc.Algorithm.pLUCO, 2))[:1 if a.quco_only else 2]:
     cfg = lc.SolverConfig(algorithm=algo, batch_size=a.B, lift_dim=2,

@@ -359,16 +359,24 @@ def measure(arm, name, precision, steps, warmup, flush, with_e2e):
     f = solver_fields(name)
     cfg = product_config(lc, f)
     g = device_graph(lc, name, arm.local)
-    independent = name == "c5"  # independent searches per rank
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=None if independent else arm.comm,
-                         batched_search=False)
-    seed_of = (lambda k: k * arm.world + arm.rank) if independent else (lambda k: k)
-    solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[f["algorithm"]]
+    independent = name == "c5"  # independent runs, one per rank per step
+    opts = lc.RunOptions(precision=prec, host_init=0, comm=arm.comm, batched_search=False)
+    if independent:
+        # the library shards the step's runs over the ranks and reduces the best cut and
+        # its assignment with one exchange (lcb_solve_runs; bench.cpp:97-136)
+        def solve(g, cfg, seed, opts):
+            r = lc.solve_runs(g, cfg, [seed * arm.world + q for q in range(arm.world)], per_component=False,
+                              opts=opts)
+            r.node_updates_total = r.node_updates
+            return r
+    else:
+        solve = {0: lc.pquco, 1: lc.pluco, 2: lc.pdeco}[f["algorithm"]]
+    seed_of = lambda k: k  # noqa: E731
     g.handle(arm.local)  # inputs resident in HBM before timing
     if independent:  # warm-up without the search (one search solve is ~10 s)
         wcfg = product_config(lc, {**f, "has_search": 0, "iterations": 50})
         for _ in range(warmup):
-            solve(g, wcfg, seed=0, opts=opts)
+            solve(g, wcfg, seed=1000, opts=opts)
     else:
         for _ in range(warmup):
             solve(g, cfg, seed=0, opts=opts)

@@ -96,6 +96,11 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
                         int32_t lifted, int64_t* cuts, int64_t* best_member, int64_t* best_cut,
                         uint8_t* best_z);
 
+/* round_unlifted (lifted == 0: z = 1{x > 0}, strict) / round_lifted (z = 1{sum_c X[v,c] >= 0}
+ * in c order, inclusive) for every member of a [B][l][n] batch (objectives.cpp:81-96);
+ * z [B][n]. */
+int lcb_round(int device, const double* values, int64_t n, int32_t l, int64_t B, int32_t lifted, uint8_t* z);
+
 /* Exhaustive MaxCut (brute_force_maxcut, oracle.hpp:18-22 / oracle.cpp:50-99) on the
  * device: Gray-code scan of the 2^(n-1) assignments with node 0 fixed.
  * - count_optimal counts z and its complement separately.
@@ -219,12 +224,19 @@ int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t 
               lcb_batch_trace* bt, int64_t bt_cap, lcb_phase_trace* pt, int64_t pt_cap,
               lcb_search_trace* st, int64_t st_cap);
 
+/* Test hook: the K2 relabelled layout of a graph (graphs with n <= 14336).  len = entries
+ * of the padded uint16 CSR (0 when the graph has none); col / col_fast [len] = CSR-order and
+ * bank-balanced copies (col_fast all 0xffff when absent); row_words [n][2] = (first
+ * 4-column word, degree) per relabelled row; perm [n] = relabelled -> original row. */
+int lcb_debug_resident_layout(const lcb_graph* g, int64_t* len, uint16_t* col, uint16_t* col_fast,
+                              int64_t* row_words, int32_t* perm);
+
 /* Independent runs (run_bench's per-seed loop, bench.cpp:97-136: one solve — or
  * solve_per_component when per_component != 0 — per seed).  With a communicator, run i is
  * solved on rank i % nranks (no member sharding inside a run), then ONE exchange: the
  * per-run cuts (allreduce max) and the best run's outcome and assignment (first maximum in
  * run order) from its owner.  run_cuts [nruns] optional; best_out / assignment [n] are
- * filled on every rank. */
+ * filled on every rank; the measurement out-params of opts sum this rank's runs. */
 int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* seeds, int64_t nruns,
                    int32_t per_component, const lcb_run_opts* opts, int64_t* run_cuts, int64_t* best_run,
                    lcb_outcome* best_out, uint8_t* assignment);

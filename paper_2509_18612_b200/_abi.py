@@ -79,6 +79,7 @@ SIGNATURES = {
     "lcb_ascend": (C.c_int, [P, P, i64, i32, i64, f64, i64, f64, i32, i32, P, P, P]),
     "lcb_cut_values": (C.c_int, [P, P, i64, P]),
     "lcb_round_cut_batch": (C.c_int, [P, P, i32, i64, i32, P, P, P, P]),
+    "lcb_round": (C.c_int, [C.c_int, P, i64, i32, i64, i32, P]),
     "lcb_brute_force_maxcut": (C.c_int, [P, i32, P, P, P]),
     "lcb_graph_from_edges": (C.c_int, [u32, P, P, i64, C.c_int, C.POINTER(P)]),
     "lcb_graph_csr": (C.c_int, [P, P, P]),
@@ -91,6 +92,7 @@ SIGNATURES = {
     "lcb_comm_create": (C.c_int, [P, i32, i32, C.c_int, C.POINTER(P)]),
     "lcb_comm_destroy": (None, [P]),
     "lcb_solve_runs": (C.c_int, [P, P, P, i64, i32, P, P, P, P, P]),
+    "lcb_debug_resident_layout": (C.c_int, [P, P, P, P, P, P]),
     "lcb_loopback_create": (C.c_int, [i32, C.POINTER(P)]),
     "lcb_loopback_destroy": (None, [P]),
     "lcb_comm_create_loopback": (C.c_int, [P, i32, C.c_int, C.POINTER(P)]),

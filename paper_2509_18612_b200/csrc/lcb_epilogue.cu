@@ -328,6 +328,23 @@ void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s)
     k_unpack_bits<<<(n + 255) / 256, 256, 0, s>>>(bits, n, z);
 }
 
+// member-major bytes z[j][v] from the member-packed bits Z[j / 32][v] (bit j % 32)
+__global__ void k_unpack_members(const uint32_t* Z, int n, int members, uint8_t* z) {
+    const int64_t total = static_cast<int64_t>(members) * n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i / n), v = static_cast<int>(i - static_cast<int64_t>(j) * n);
+        z[i] = static_cast<uint8_t>((Z[static_cast<int64_t>(j >> 5) * n + v] >> (j & 31)) & 1u);
+    }
+}
+
+void launch_unpack_members(const uint32_t* Z, int n, int members, uint8_t* z, cudaStream_t s) {
+    const int64_t total = static_cast<int64_t>(members) * n;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 4096));
+    count_launch();
+    k_unpack_members<<<blocks, 256, 0, s>>>(Z, n, members, z);
+}
+
 // loopback exchange: out[i] = op over rows r of rows[r][i] (u32 / u64, max / min)
 template <typename U, bool MAX>
 __global__ void k_reduce_rows(const U* rows, int nrows, size_t count, U* out) {

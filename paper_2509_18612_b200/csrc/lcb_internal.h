@@ -74,6 +74,7 @@ struct DevGraph {
     int* res_chunk = nullptr;     // [ceil((n-heavy)/1024)] chunk base (4-col words)
     int* res_heavy = nullptr;     // [heavy][2] absolute word offset, degree
     int res_nheavy = 0;
+    int64_t res_len = 0;          // entries of res_col / res_col_fast
     uint16_t* res_col = nullptr;  // [padded nnz]
     uint16_t* res_col_fast = nullptr;  // fp32 copy, light rows in bank-balanced order (or null)
     void* dense_A = nullptr;      // bf16 [n][roundup(n,8)] adjacency for the tensor-core path (dense graphs)
@@ -209,6 +210,8 @@ void launch_extract_winner(const uint32_t* Z, int n, const unsigned long long* k
                            int64_t member_base, int members, uint32_t* bits, cudaStream_t s,
                            int member_offset = 0);
 void launch_unpack_bits(const uint32_t* bits, int n, uint8_t* z, cudaStream_t s);
+// z[j][v] (bytes, member-major) from the member-packed Z[j / 32][v]
+void launch_unpack_members(const uint32_t* Z, int n, int members, uint8_t* z, cudaStream_t s);
 // out[i] = max / min over the nrows rows of rows[nrows][count] (bytes = 4 or 8 per element)
 void launch_reduce_rows(const void* rows, int nrows, size_t count, int bytes, bool is_max, void* out, cudaStream_t s);
 

@@ -498,7 +498,9 @@ bool resident_fits(int n, int W, int l, bool ee, int elem_bytes, int& K) {
     if (n > kResidentMaxRows) return false;
     const int64_t rows = static_cast<int64_t>(n) + 1;
     K = 1;
-    if (elem_bytes == 4 && W / 2 >= 148 && rows * 2 * 4 * 2 <= kResidentSmemMax) K = 2;
+    // K = 2 columns per CTA from 2 x 148 columns on; with early exit and l = 2 always (both
+    // columns of a member in one CTA for the per-member exit test, at any W)
+    if (elem_bytes == 4 && (W / 2 >= 148 || (ee && l == 2)) && rows * 2 * 4 * 2 <= kResidentSmemMax) K = 2;
     // (fp64 / fp32 share the relabelled layout; heavy rows are the first `heavy` rows)
     if (rows * K * elem_bytes * 2 > kResidentSmemMax) return false;
     if (ee && (K % l) != 0) return false;  // a member's columns must share a CTA

@@ -527,6 +527,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             h2d(g.res_heavy, hinfo.data(), sizeof(int) * hinfo.size(), 0);
             g.res_nheavy = H;
             h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
+            g.res_len = static_cast<int64_t>(rcol.size());
             if (!fast.empty()) {
                 CK(cudaMalloc(&g.res_col_fast, sizeof(uint16_t) * fast.size()));
                 h2d(g.res_col_fast, fast.data(), sizeof(uint16_t) * fast.size(), 0);
@@ -734,6 +735,7 @@ struct Work {
         if (st) cudaStreamSynchronize(st);
         if (h_keys) cudaFreeHost(h_keys);
         if (h_flags) cudaFreeHost(h_flags);
+        if (h_stage) cudaFreeHost(h_stage);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st) cudaStreamDestroy(st);
@@ -745,6 +747,18 @@ struct Work {
         X[0].ensure(cells);
         X[1].ensure(cells);
         V.ensure(cells);
+    }
+    double* h_stage = nullptr;  // pinned host staging of host-generated batches
+    size_t h_stage_cap = 0;
+    double* host_stage(size_t k) {
+        if (k > h_stage_cap) {
+            if (h_stage) cudaFreeHost(h_stage);
+            h_stage = nullptr;
+            h_stage_cap = 0;
+            CK(cudaMallocHost(&h_stage, sizeof(double) * k));
+            h_stage_cap = k;
+        }
+        return h_stage;
     }
     uint32_t* host_flags(size_t k) {
         if (k > h_flags_cap) {
@@ -804,13 +818,15 @@ struct PooledWork {
 // Kernel choice measured on B200 (profiles/round1_kernel_ab.md): the member-resident
 // kernel wins when the on-chip slab covers the graph and the batch is wide enough to
 // fill several waves (W >= 1024 columns at K=2, any W for fp64 / small graphs).
+// fp32 takes K2 whenever the slab fits, at any batch width: K2 sums each row in its own
+// (bank-balanced) neighbour order, so choosing the kernel by W would make a member's fp32
+// trajectory depend on the batch width and the rank count (test_ascent.cpp:110-136).
 bool resident_preferred(const DevGraph& g, int W, size_t elem) {
+    (void)g;
+    (void)W;
+    (void)elem;
     const int64_t mode = option(OPT_RESIDENT);  // -1 auto, 0 never, 1 always (when it fits)
-    if (mode == 0) return false;
-    if (mode == 1) return true;
-    if (elem == 8) return true;
-    if (g.n <= 2048) return true;  // whole batch on chip, launch-latency bound otherwise
-    return W >= 1024;  // with the bank-balanced order: W=1024 48.1 vs 51.2 us/iteration (K1)
+    return mode != 0;
 }
 
 struct IterResult {
@@ -1300,20 +1316,35 @@ struct Solver {
     void host_batch(const std::vector<double>& mean, int l, const std::vector<uint64_t>& mkeys, double noise) {
         const int n = g.n;
         const size_t entries = static_cast<size_t>(n) * l;
-        std::vector<double> vals(entries * mkeys.size());
-        for (size_t j = 0; j < mkeys.size(); ++j) {
-            HostStream ms{mkeys[j]};
-            double* o = vals.data() + j * entries;
-            for (size_t k = 0; k < entries; ++k) {
-                const double x = mean[k] + noise * ms.normal();
-                o[k] = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+        const size_t total = entries * mkeys.size();
+        // members on host threads, as the reference's parallel_for over members (init.cpp:78-86);
+        // each member's stream is independent, so the bits do not depend on the split
+        double* vals = w.host_stage(total);
+        auto gen = [&](size_t j0, size_t j1) {
+            for (size_t j = j0; j < j1; ++j) {
+                HostStream ms{mkeys[j]};
+                double* o = vals + j * entries;
+                for (size_t k = 0; k < entries; ++k) {
+                    const double x = mean[k] + noise * ms.normal();
+                    o[k] = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+                }
             }
+        };
+        const size_t B = mkeys.size();
+        const size_t nt = std::min<size_t>(B, std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+        if (nt <= 1 || total < (1u << 16)) {
+            gen(0, B);
+        } else {
+            std::vector<std::thread> th;
+            for (size_t t = 1; t < nt; ++t) th.emplace_back(gen, B * t / nt, B * (t + 1) / nt);
+            gen(0, B / nt);
+            for (auto& t : th) t.join();
         }
-        double* d = w.hostbatch.ensure(vals.size());
-        h2d(d, vals.data(), sizeof(double) * vals.size(), w.st);
+        double* d = w.hostbatch.ensure(total);
+        h2d(d, vals, sizeof(double) * total, w.st);
         launch_transpose_in<T>(d, w.X[0].p, n, static_cast<int>(mkeys.size() * l), w.ld, w.st);
         CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(n) * w.ld, w.st));
-        CK(cudaStreamSynchronize(w.st));  // vals is pageable and goes out of scope
+        CK(cudaStreamSynchronize(w.st));  // the pinned stage is reused by the next batch
     }
 
     // batch init around a device mean or pm1(bits): glibc normals on the host or the
@@ -2263,6 +2294,31 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
     });
 }
 
+int lcb_round(int device, const double* values, int64_t n, int32_t l, int64_t B, int32_t lifted, uint8_t* z) {
+    return guard([&] {
+        if (!values || !z) fail(LCB_VALIDATION, "null argument");
+        if (n < 1 || l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+        if (static_cast<int64_t>(l) * B > (1 << 26) || n > 0x7fffffff) fail(LCB_VALIDATION, "batch too wide");
+        DeviceScope ds(device);
+        PooledWork<double> pw(device);
+        Work<double>& w = *pw;
+        const int W = static_cast<int>(B * l), N = static_cast<int>(n);
+        w.shape(N, W);
+        const size_t cells = static_cast<size_t>(W) * N;
+        double* d = w.hostbatch.ensure(cells);
+        h2d(d, values, sizeof(double) * cells, w.st);
+        launch_transpose_in<double>(d, w.X[0].p, N, W, w.ld, w.st);
+        const int words = static_cast<int>((B + 31) / 32);
+        uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * N);
+        launch_round_pack<double>(w.X[0].p, w.ld, N, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
+        uint8_t* dz = reinterpret_cast<uint8_t*>(w.Y.ensure((static_cast<size_t>(B) * N + 7) / 8));
+        launch_unpack_members(Z, N, static_cast<int>(B), dz, w.st);
+        d2h(z, dz, static_cast<size_t>(B) * N, w.st);
+        CK(cudaStreamSynchronize(w.st));
+        CK(cudaGetLastError());
+    });
+}
+
 static void init_mean_host(const DevGraph& G, int method, double beta, int l, const uint64_t* ck,
                            double scale, double* out) {
     DeviceScope ds(G.device);
@@ -2346,6 +2402,42 @@ int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t 
     });
 }
 
+int lcb_debug_resident_layout(const lcb_graph* g, int64_t* len, uint16_t* col, uint16_t* col_fast,
+                              int64_t* row_words, int32_t* perm) {
+    return guard([&] {
+        if (!g || !len) fail(LCB_VALIDATION, "null argument");
+        const DevGraph& G = g->g;
+        *len = G.res_info ? G.res_len : 0;
+        if (!G.res_info) return;
+        DeviceScope ds(G.device);
+        if (col) CK(cudaMemcpy(col, G.res_col, sizeof(uint16_t) * G.res_len, cudaMemcpyDeviceToHost));
+        if (col_fast) {
+            if (G.res_col_fast)
+                CK(cudaMemcpy(col_fast, G.res_col_fast, sizeof(uint16_t) * G.res_len, cudaMemcpyDeviceToHost));
+            else
+                std::memset(col_fast, 0xff, sizeof(uint16_t) * G.res_len);
+        }
+        if (perm) CK(cudaMemcpy(perm, G.res_perm, sizeof(int) * G.n, cudaMemcpyDeviceToHost));
+        if (row_words) {  // relabelled row r: (first 4-column word, degree)
+            const int H = G.res_nheavy;
+            std::vector<int> hi(static_cast<size_t>(2 * std::max(H, 1)));
+            std::vector<uint32_t> info(static_cast<size_t>(std::max(G.n - H, 1)));
+            CK(cudaMemcpy(hi.data(), G.res_heavy, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(info.data(), G.res_info, sizeof(uint32_t) * info.size(), cudaMemcpyDeviceToHost));
+            for (int r = 0; r < G.n; ++r) {
+                if (r < H) {
+                    row_words[2 * r] = hi[static_cast<size_t>(2 * r)];
+                    row_words[2 * r + 1] = hi[static_cast<size_t>(2 * r + 1)];
+                } else {
+                    const uint32_t pk = info[static_cast<size_t>(r - H)];
+                    row_words[2 * r] = pk >> 8;
+                    row_words[2 * r + 1] = pk & 0xffu;
+                }
+            }
+        }
+    });
+}
+
 int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* seeds, int64_t nruns,
                    int32_t per_component, const lcb_run_opts* opts, int64_t* run_cuts, int64_t* best_run,
                    lcb_outcome* best_out, uint8_t* assignment) {
@@ -2367,13 +2459,31 @@ int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* se
         std::vector<uint8_t> z(static_cast<size_t>(G.n)), zbest(static_cast<size_t>(G.n), 0);
         lcb_outcome local_best{};
         int64_t local_run = -1, local_cut = -1;
+        // measurement out-params accumulate over this rank's runs
+        double acc_step_ms = 0, acc_bytes = 0, acc_solve_ms = 0, acc_k[12] = {0};
+        int64_t acc_launches = 0, acc_updates = 0;
         for (int64_t i = rk; i < nruns; i += nr) {
             lcb_outcome out{};
             TraceSinks sinks{nullptr, 0, nullptr, 0, nullptr, 0};
+            double r_step_ms = 0, r_bytes = 0, r_solve_ms = 0, r_k[12] = {0};
+            int64_t r_launches = 0, r_updates = 0;
+            lcb_run_opts ro = o;
+            ro.step_ms = &r_step_ms;
+            ro.step_bytes = &r_bytes;
+            ro.solve_ms = &r_solve_ms;
+            ro.kernel_stats = r_k;
+            ro.step_launches = &r_launches;
+            ro.node_updates = &r_updates;
             if (o.precision == LCB_FP32)
-                solve_top<float>(G, *cfg, seeds[i], per_component, o, out, z.data(), sinks);
+                solve_top<float>(G, *cfg, seeds[i], per_component, ro, out, z.data(), sinks);
             else
-                solve_top<double>(G, *cfg, seeds[i], per_component, o, out, z.data(), sinks);
+                solve_top<double>(G, *cfg, seeds[i], per_component, ro, out, z.data(), sinks);
+            acc_step_ms += r_step_ms;
+            acc_bytes += r_bytes;
+            acc_solve_ms += r_solve_ms;
+            acc_launches += r_launches;
+            acc_updates += r_updates;
+            for (int k = 0; k < 12; ++k) acc_k[k] += r_k[k];
             enc[static_cast<size_t>(i)] = static_cast<unsigned long long>(out.cut_value) + 1ull;
             if (out.cut_value > local_cut) {
                 local_cut = out.cut_value;
@@ -2422,6 +2532,12 @@ int lcb_solve_runs(const lcb_graph* g, const lcb_config* cfg, const uint64_t* se
         if (run_cuts)
             for (int64_t i = 0; i < nruns; ++i) run_cuts[i] = static_cast<int64_t>(enc[static_cast<size_t>(i)]) - 1;
         if (best_run) *best_run = win;
+        if (o.step_ms) *o.step_ms = acc_step_ms;
+        if (o.step_bytes) *o.step_bytes = acc_bytes;
+        if (o.solve_ms) *o.solve_ms = acc_solve_ms;
+        if (o.step_launches) *o.step_launches = acc_launches;
+        if (o.node_updates) *o.node_updates = acc_updates;
+        if (o.kernel_stats) std::memcpy(o.kernel_stats, acc_k, sizeof(acc_k));
     });
 }
 

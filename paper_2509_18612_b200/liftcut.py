@@ -532,16 +532,22 @@ def cut_values(g: Graph, Z) -> np.ndarray:
     return out
 
 
+def _round(values, n: int, l: int, B: int, lifted: bool) -> np.ndarray:
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    z = np.zeros(B * n, dtype=np.uint8)
+    _check(_abi.lib().lcb_round(default_device(), _ptr(v), n, l, B, int(lifted), _ptr(z)))
+    return z
+
+
 def round_unlifted(x) -> np.ndarray:
-    return (np.asarray(x) > 0.0).astype(np.uint8)
+    """z = 1{x > 0}, strict (objectives.cpp:81-86), on the device (lcb_round)."""
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
+    return _round(x, len(x), 1, 1, False)
 
 
 def round_lifted(state: DenseState, member: int = 0) -> np.ndarray:
-    m = state.member(member).reshape(state.lift_dim, state.nodes)
-    s = np.zeros(state.nodes)
-    for c in range(state.lift_dim):  # column order, as objectives.cpp:92
-        s = s + m[c]
-    return (s >= 0.0).astype(np.uint8)
+    """z = 1{sum_c X[v, c] >= 0} with the row sum in column order (objectives.cpp:88-96)."""
+    return _round(state.member(member), state.nodes, state.lift_dim, 1, True)
 
 
 def round_cut_batch(g: Graph, state: DenseState, lifted: bool):
@@ -881,12 +887,19 @@ def _solve(g: Graph, cfg: SolverConfig, seed: int, per_component: bool, algo: Al
 
 @dataclass
 class RunsOutcome:
-    """solve_runs: every run's best cut and the best run (first maximum in run order)."""
+    """solve_runs: every run's best cut and the best run (first maximum in run order);
+    measurement fields sum this rank's runs."""
     run_cuts: np.ndarray
     best_run: int
     best: CutSolution
     stage_times: StageTimes
     batches_run: int
+    step_ms: float = 0.0
+    step_launches: int = 0
+    node_updates: int = 0
+    step_bytes: float = 0.0
+    solve_ms: float = 0.0
+    kernel_stats: dict = field(default_factory=dict)
 
 
 def solve_runs(g: Graph, cfg: SolverConfig, seeds, per_component: bool = True,
@@ -898,9 +911,18 @@ def solve_runs(g: Graph, cfg: SolverConfig, seeds, per_component: bool = True,
     opts = opts or RunOptions()
     seeds = np.ascontiguousarray([int(s) & _M64 for s in seeds], dtype=np.uint64)
     c = cfg.to_abi()
+    step_ms, step_bytes, solve_ms = C.c_double(0), C.c_double(0), C.c_double(0)
+    kst = (C.c_double * 12)()
+    launches, nupd = C.c_int64(0), C.c_int64(0)
     ro = _abi.RunOpts(precision=default_precision() if opts.precision is None else opts.precision,
                       host_init=opts.host_init, batched_search=int(opts.batched_search),
-                      comm=opts.comm.handle if opts.comm is not None else None)
+                      comm=opts.comm.handle if opts.comm is not None else None,
+                      step_ms=C.cast(C.byref(step_ms), C.c_void_p),
+                      step_launches=C.cast(C.byref(launches), C.c_void_p),
+                      node_updates=C.cast(C.byref(nupd), C.c_void_p),
+                      step_bytes=C.cast(C.byref(step_bytes), C.c_void_p),
+                      solve_ms=C.cast(C.byref(solve_ms), C.c_void_p),
+                      kernel_stats=C.cast(kst, C.c_void_p))
     cuts = np.zeros(len(seeds), dtype=np.int64)
     best_run = C.c_int64(-1)
     out = _abi.Outcome()
@@ -911,7 +933,10 @@ def solve_runs(g: Graph, cfg: SolverConfig, seeds, per_component: bool = True,
     b = best_run.value
     return RunsOutcome(cuts, b, CutSolution(z, out.cut_value, algorithm_to_string(Algorithm(cfg.algorithm)),
                                             int(seeds[b]), out.batch_index, out.member_index, out.wall_s),
-                       StageTimes(out.init_s, out.ascent_s, out.rounding_s, out.search_s), out.batches_run)
+                       StageTimes(out.init_s, out.ascent_s, out.rounding_s, out.search_s), out.batches_run,
+                       step_ms.value, launches.value, nupd.value, step_bytes.value, solve_ms.value,
+                       {"k_step": tuple(kst[0:3]), "k_resident": tuple(kst[3:6]), "k_dense_step": tuple(kst[6:9]),
+                        "k_stream": tuple(kst[9:12])})
 
 
 def set_option(name: str, value: int) -> None:

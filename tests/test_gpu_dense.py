@@ -18,9 +18,10 @@ res = {}
 cg = O.generate_er(600, 0.5, 3)
 g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
 g.handle()                                   # dense adjacency built (LCB_DENSE=1)
-os.environ["LCB_DENSE"] = "0"
+lc.set_option("dense", 0)
 g_csr = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
 g_csr.handle()                               # same graph on the CSR (K1/K2) fp32 path
+lc.set_option("dense", 1)
 rng = np.random.default_rng(0)
 for (l, B) in [(1, 64), (1, 256), (2, 100), (1, 320)]:
     x = rng.choice([-1e-4, 1e-4], B * l * cg.n) + rng.normal(0, 9e-5, B * l * cg.n)
@@ -69,6 +70,7 @@ def test_dense_tensor_core_path_matches_oracle(sms):
         # cuts at T=200 must agree with fp64.
         for T in ("1", "4"):
             assert v["err"][T] <= 1e-5, (k, T, v)
+            assert v["err_csr"][T] <= 1e-5, (k, T, v)
         assert v["err"]["10"] <= 1e-3, (k, v)
         assert v["same"] >= 0.97 and v["d"] <= 2, (k, v)
 
@@ -105,3 +107,48 @@ def test_dense_e4m3_units_match_bf16_planes():
     assert a["cuts"] == b["cuts"]
     import numpy as np
     assert float(np.max(np.abs(np.array(a["x"]) - np.array(b["x"])))) <= 1e-5
+
+
+BIG_CODE = r"""
+import json, numpy as np
+from paper_2509_18612_b200 import liftcut as lc, LCB_FP32, LCB_FP64
+# config-3 scale: ER n=20000 p=0.5 (157 row tiles of 128: one full wave of 148 + a 9-tile
+# split-K tail), W=256 = one N=256 column chunk
+g = lc.generate_er_device(20000, 0.5, 0)
+n, B = 20000, 256
+rng = np.random.default_rng(0)
+x = rng.choice([-1e-4, 1e-4], B * n) + rng.normal(0, 9e-5, B * n)
+res = {}
+A = 0.0003  # alpha * degree ~ 3, as in the n=600 test above
+for T in (1, 4):
+    s32 = lc.DenseState(n, 1, B); s32.values[:] = x
+    lc.ascend(g, s32, lc.AscentParams(A, T, 0.9, False), precision=LCB_FP32)     # K3 (dense A)
+    s64 = lc.DenseState(n, 1, B); s64.values[:] = x
+    lc.ascend(g, s64, lc.AscentParams(A, T, 0.9, False), precision=LCB_FP64)     # CSR fp64, bit-exact path
+    e = 0.0
+    for j in range(B):
+        a, b = s32.values[j*n:(j+1)*n], s64.values[j*n:(j+1)*n]
+        e = max(e, float(np.max(np.abs(a - b)) / np.max(np.abs(b))))
+    res[str(T)] = e
+T = 60
+s32 = lc.DenseState(n, 1, B); s32.values[:] = x
+lc.ascend(g, s32, lc.AscentParams(A, T, 0.9, False), precision=LCB_FP32)
+s64 = lc.DenseState(n, 1, B); s64.values[:] = x
+lc.ascend(g, s64, lc.AscentParams(A, T, 0.9, False), precision=LCB_FP64)
+c32, _, _, _ = lc.round_cut_batch(g, s32, lifted=False)
+c64, _, _, _ = lc.round_cut_batch(g, s64, lifted=False)
+res["same"] = float(np.mean(c32 == c64)); res["d"] = int(c64.max() - c32.max())
+print("RESULT" + json.dumps(res))
+"""
+
+
+def test_dense_config3_scale_split_k_tail_vs_fp64():
+    """K3 at config-3 size (157 tiles: full wave + split-K tail, N=256, e4m3 units once the
+    iterate saturates) against the fp64 CSR path (bit-exact with the oracle)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", BIG_CODE], cwd=root, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    res = json.loads(r.stdout.split("RESULT")[1])
+    print(res)
+    assert res["1"] <= 1e-5 and res["4"] <= 1e-5, res
+    assert res["same"] >= 0.97 and res["d"] <= 2, res

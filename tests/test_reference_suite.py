@@ -1,7 +1,9 @@
-"""The reference's OWN unit tests (proj/tests/test_*.cpp, unchanged), compiled against
-the B200 drop-in (paper_2509_18612_b200/dropin: ascent.cpp / init.cpp / oracle.cpp /
-solver.cpp replaced by libliftcut_b200.so-backed files behind the unchanged reference headers)
-with the doctest-compatible harness in tests/refsuite/doctest.h.
+"""The reference's OWN unit tests (proj/tests/test_*.cpp, unchanged) and its acceptance gate
+(acceptance_main.cpp, criteria 1-9), compiled against the B200 drop-in
+(paper_2509_18612_b200/dropin: ascent.cpp / init.cpp / oracle.cpp / solver.cpp /
+objectives.cpp and Graph::laplacian_apply replaced by libliftcut_b200.so-backed files behind
+the unchanged reference headers) with the doctest-compatible harness in
+tests/refsuite/doctest.h.
 
 The binary is built where /root/reference exists (`make -C paper_2509_18612_b200/dropin
 tests`, also run by __graft_entry__.build()) and travels to the GPU box prebuilt.
@@ -13,6 +15,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "dropin", "ref_unit_tests")
+ACC = os.path.join(ROOT, "build", "dropin", "acceptance")
 needs_bin = pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in reference suite not built")
 
 
@@ -24,13 +27,14 @@ def run_suites(suites, env=None, exclude=None):
 
 @needs_bin
 def test_reference_suites_on_kept_host_code():
-    code, out = run_suites(["rng", "parallel", "graph", "objectives", "evo"])
+    code, out = run_suites(["rng", "parallel", "evo", "presets"])
     assert code == 0, out[-3000:]
 
 
 @needs_bin
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["ascent", "init", "oracle", "solver"])
+@pytest.mark.parametrize("suite", ["ascent", "init", "oracle", "solver", "graph", "objectives", "records",
+                                   "bench"])
 def test_reference_suite_against_b200_dropin(suite):
     code, out = run_suites([suite])
     assert code == 0 and "0 failed" in out, out[-4000:]
@@ -46,3 +50,13 @@ def test_reference_ascent_suite_fp32_fast_path():
     code, out = run_suites(["ascent"], env={"LIFTCUT_PRECISION": "fp32"},
                            exclude="scaled constant vectors never move")
     assert code == 0, out[-4000:]
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="drop-in acceptance gate not built")
+@pytest.mark.gpu
+def test_reference_acceptance_gate_against_b200_dropin():
+    """acceptance_main.cpp (criteria 1-9: exhaustive-oracle agreement, fixed points, the
+    ER(700) cut bar, determinism, ...) linked against the drop-in."""
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=1800)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]

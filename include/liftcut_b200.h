@@ -46,10 +46,11 @@ int lcb_device_count(int* count);
 
 /* Kernel-selection knobs (no reference counterpart; B200 tuning and tests).  Names:
  * "resident" (K2: -1 auto, 0 never, 1 whenever it fits), "stream" (K1s streaming step:
- * 1 on, 0 off), "signrec" (K1 saturation codes: -1 auto, 0, 1), "chunk" (K1n panels:
+ * -1 auto, 1 on, 0 off), "signrec" (K1 saturation codes: -1 auto, 0, 1), "chunk" (K1n panels:
  * 0 off, 1 on, -1 auto), "res_split" (K2 wave-tail split), "bank_order" / "bank_refine"
  * (K2 fp32 neighbour order, read at graph creation), "dense" (K3 adjacency at graph
- * creation: -1 auto, 0, 1).  Defaults come from the LCB_<NAME> environment variables.
+ * creation: -1 auto, 0, 1), "slab_outer" (K1s order: -1 auto, 0 all slabs per launch, 1 one
+ * slab at a time for all iterations).  Defaults come from the LCB_<NAME> environment variables.
  * Changing a knob while a solve runs in another thread is not supported. */
 int lcb_set_option(const char* name, int64_t value);
 int lcb_get_option(const char* name, int64_t* value);

@@ -245,13 +245,14 @@ void ensure_smem_attr(const void* kernel, int bytes, const char* what);
 // variable at first use and at run time by lcb_set_option (tests, A/B runs).
 enum Opt : int {
     OPT_RESIDENT = 0,  // K2: -1 auto, 0 never, 1 whenever the slab fits
-    OPT_STREAM,        // K1s for the HBM-streaming step: 1 on, 0 K1
+    OPT_STREAM,        // K1s for the HBM-streaming step: -1 auto, 1 on, 0 K1
     OPT_SIGNREC,       // K1 saturation codes: -1 auto (iterate > L2), 0 off, 1 on
     OPT_CHUNK,         // K1n L2 panels: 0 off, 1 always, -1 auto
     OPT_RES_SPLIT,     // K2 wave-tail split into a K=1 launch
     OPT_BANK_ORDER,    // K2 fp32 neighbour order at graph creation: 0 CSR, 1 warp, 2 half-warp
     OPT_BANK_REFINE,   // refinement passes of that order
     OPT_DENSE,         // K3 adjacency at graph creation: -1 auto, 0 never, 1 always
+    OPT_SLAB_OUTER,    // K1s order: -1 auto (codes beyond L2), 0 iteration-major, 1 slab-major
     OPT_COUNT
 };
 int64_t option(Opt o);

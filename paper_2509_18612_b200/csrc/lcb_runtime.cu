@@ -75,9 +75,9 @@ struct OptDef {
     int64_t def;
 };
 constexpr OptDef kOptDefs[OPT_COUNT] = {
-    {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", 0},         {"signrec", "LCB_SIGNREC", -1},
+    {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", -1},        {"signrec", "LCB_SIGNREC", -1},
     {"chunk", "LCB_CHUNK", 0},        {"res_split", "LCB_RES_SPLIT", 1},   {"bank_order", "LCB_BANK_ORDER", 2},
-    {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1},
+    {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1}, {"slab_outer", "LCB_SLAB_OUTER", -1},
 };
 std::atomic<int64_t> g_opts[OPT_COUNT];
 std::once_flag g_opts_once;
@@ -1041,8 +1041,20 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     // slab-outer order (all iterations of one slab before the next: members are independent,
     // ascent.cpp:52, so the slab's codes stay L2-resident across iterations) unless early exit
     // needs every column of a member in the same launch
-    const bool slab_outer = !ee || sspan % l == 0;
-    const bool use_stream = stream_mode != 0 && !trace_host && step_span<T>(W) == sspan && w.ld % sspan == 0 &&
+    // ... and only when the codes of all slabs would not stay in L2 anyway (config 4: 4 x 32 MB;
+    // config 5: 2 x 3.2 MB -> one launch per iteration over both slabs, twice the tiles per launch)
+    static const int64_t l2b = [] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
+        return static_cast<int64_t>(v > 0 ? v : (126 << 20));
+    }();
+    const int64_t so = option(OPT_SLAB_OUTER);
+    const bool slab_outer = (!ee || sspan % l == 0) && nslabs > 1 &&
+                            (so == 1 || (so < 0 && static_cast<int64_t>(g.n) * 32 * nslabs * 2 > l2b / 2));
+    // auto (-1): K1s where its slab-major order keeps the codes on chip (config 4); K1 where the
+    // iterate itself is L2-resident (config 5: 166 vs 208 us/iteration for K1s)
+    const bool use_stream = (stream_mode == 1 || (stream_mode < 0 && slab_outer)) && !trace_host &&
+                            step_span<T>(W) == sspan && w.ld % sspan == 0 &&
                             static_cast<int64_t>(g.n) * 32 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
     static const int64_t l2_bytes = [] {
         int v = 0;

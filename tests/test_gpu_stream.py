@@ -26,10 +26,10 @@ def pg(c):
     return lc.Graph.from_csr(c.n, c.off, c.adj)
 
 
-def run(g, x, n, l, B, alpha, T, mu, ee, prec):
+def run(g, x, n, l, B, alpha, T, mu, ee, prec, slab_outer=-1):
     s = lc.DenseState(n, l, B)
     s.values[:] = x
-    with lc.options(resident=0, stream=1, chunk=0):
+    with lc.options(resident=0, stream=1, chunk=0, slab_outer=slab_outer):
         lc.ascend(g, s, lc.AscentParams(alpha, T, mu, ee), precision=prec)
     return s.values
 
@@ -53,15 +53,16 @@ def start(rng, n, l, B):
     return rng.choice([-1e-4, 1e-4], B * l * n) + rng.normal(0, 9e-5, B * l * n)
 
 
+@pytest.mark.parametrize("slab_outer", [0, 1])
 @pytest.mark.parametrize("l,B,ee", [(1, 100, False), (1, 100, True), (2, 70, False), (2, 70, True),
-                                    (3, 45, False), (1, 300, False)])
-def test_stream_fp64_bitwise_through_saturation(l, B, ee):
-    cg = ba_like(2600, 4, 3)          # hubs (degree > 100), BA skew: degree-ordered rows
+                                    (3, 45, False), (3, 45, True), (1, 300, False)])
+def test_stream_fp64_bitwise_through_saturation(l, B, ee, slab_outer):
+    cg = ba_like(2600, 4, 3)          # hubs (degree > 100), BA skew
     rng = np.random.default_rng(l * 100 + B)
     x = start(rng, cg.n, l, B)
     for T in (1, 7, 60):              # 60: well past saturation -> code path
         want, _ = O.ascend(cg, x, l, B, 0.05, T, 0.9, ee)
-        got = run(pg(cg), x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP64)
+        got = run(pg(cg), x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP64, slab_outer)
         assert np.array_equal(got, want), (l, B, ee, T)
 
 
@@ -115,13 +116,14 @@ def test_stream_fp32_tolerance_and_cuts(l, B):
     assert int(c32.max()) >= int(c64.max()) - 2
 
 
-def test_stream_batched_search_bitwise():
+@pytest.mark.parametrize("slab_outer", [0, 1])
+def test_stream_batched_search_bitwise(slab_outer):
     """Per-member alpha / T and the shrinking live width of batched evolve() rounds
     (GEN variant, early exit on) through K1s: sequential == batched == oracle."""
     cg = O.generate_er(300, 0.03, 3)
     cfg = lc.SolverConfig(batch_size=64, num_batches=2, ascent=lc.AscentParams(0.05, 60),
                           search=lc.SearchConfig(20, 80, -3.0, -1.0, 6, 3))
-    with lc.options(resident=0, stream=1):
+    with lc.options(resident=0, stream=1, slab_outer=slab_outer):
         a = lc.pquco(pg(cg), cfg, 11, opts=lc.RunOptions(precision=LCB_FP64, batched_search=False))
         b = lc.pquco(pg(cg), cfg, 11, opts=lc.RunOptions(precision=LCB_FP64, batched_search=True))
     assert a.kernel_stats["k_stream"][1] > 0 and a.kernel_stats["k_resident"][1] == 0

@@ -349,7 +349,7 @@ def device_graph(lc, name, device):
 KERNELS = ("k_step", "k_resident", "k_dense_step", "k_stream")
 
 
-def measure(arm, name, precision, steps, warmup, flush, with_e2e):
+def measure(arm, name, precision, steps, warmup, flush, with_e2e, host_init=0):
     import torch  # noqa: F401
 
     from paper_2509_18612_b200 import LCB_FP32, LCB_FP64
@@ -360,7 +360,7 @@ def measure(arm, name, precision, steps, warmup, flush, with_e2e):
     cfg = product_config(lc, f)
     g = device_graph(lc, name, arm.local)
     independent = name == "c5"  # independent runs, one per rank per step
-    opts = lc.RunOptions(precision=prec, host_init=0, comm=arm.comm, batched_search=False)
+    opts = lc.RunOptions(precision=prec, host_init=host_init, comm=arm.comm, batched_search=False)
     if independent:
         # the library shards the step's runs over the ranks and reduces the best cut and
         # its assignment with one exchange (lcb_solve_runs; bench.cpp:97-136)
@@ -475,12 +475,15 @@ def run_b200(args):
 
     extras = []
     if world == 1 and args.extras and args.config == DEFAULT_CONFIG:
-        plan = [("c2", "fp32", 3, 3), ("c3", "fp32", 3, 3), ("c5", "fp32", 1, 1), ("c4", "fp64", 2, 3)]
-        for name, prec, steps, warm in plan:
+        # (config, precision, steps, warm-up, host_init): the fp64 line runs the library's default
+        # bit-exact mode (glibc normals drawn on the host, threaded over members)
+        plan = [("c2", "fp32", 3, 3, 0), ("c3", "fp32", 3, 3, 0), ("c5", "fp32", 1, 1, 0), ("c4", "fp64", 2, 3, -1)]
+        for name, prec, steps, warm, hinit in plan:
             t0 = time.perf_counter()
             try:
-                r = measure(arm, name, prec, steps, warm, flush, with_e2e=False)
+                r = measure(arm, name, prec, steps, warm, flush, with_e2e=False, host_init=hinit)
                 extras.append({"config_id": name, "precision": prec, "steps": steps, "warmup": warm,
+                               "init": "host glibc normals (bit-exact mode)" if hinit else "device normals",
                                "workload": WORKLOADS[name]["desc"], "value": r["value"], "unit": UNIT,
                                "ms_per_step": r["ms_per_step"], "best_cut": r["best_cut"], "dtype": r["dtype"],
                                "roofline_frac": r["roofline"]["frac"], "roofline": r["roofline"],

@@ -117,6 +117,7 @@ struct StepArgs {
     const uint8_t* sgn_in;      // codes of x_in, or nullptr (first iteration of a loop)
     uint8_t* sgn_out;           // codes of x_out, or nullptr (not recorded)
     int64_t sgn_ld;             // bytes per row: (ld / span) * 32
+    int64_t flag_off;           // K1s: byte offset of the per-row slab flags after the sign codes
 };
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
@@ -176,11 +177,13 @@ template <typename T>
 void launch_step(const StepArgs<T>& a, bool early_exit, int mode, cudaStream_t s);
 template <typename T>
 int step_span(int W);  // columns covered by one warp for this W
-// K1s (lcb_stream.cu): warp-specialised streaming step over the 512-byte column slabs
-// [slab0, slab0 + nslabs) for one iteration; saturation codes of those slabs are
-// [nslabs][n][32] bytes (< 4 GB) at sgn_in / sgn_out (sgn_ld unused)
+// K1s (lcb_stream.cu): warp-specialised streaming step over the 1 KB column slabs
+// [slab0, slab0 + nslabs) for one iteration; sgn_in / sgn_out hold the slabs' sign codes
+// [nslabs][n][32] bytes followed by their per-row "not saturated" flags [nslabs][n] u32
+// (< 4 GB; sgn_ld unused)
 template <typename T>
 void launch_stream(const StepArgs<T>& a, int slab0, int nslabs, bool early_exit, cudaStream_t s);
+int stream_slab_cols(int elem_bytes);  // columns of one K1s slab (1 KB of a row)
 
 template <typename T>
 void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s);

@@ -741,7 +741,8 @@ struct Work {
         if (st) cudaStreamDestroy(st);
     }
     void shape(int n, int W) {
-        const int span = step_span<T>(W);
+        // rows padded to the K1 warp span and to the 1 KB K1s slab
+        const int span = std::max(step_span<T>(W), stream_slab_cols(static_cast<int>(sizeof(T))));
         ld = ((static_cast<int64_t>(W) + span - 1) / span) * span;
         const size_t cells = static_cast<size_t>(n) * static_cast<size_t>(ld);
         X[0].ensure(cells);
@@ -1036,7 +1037,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     const int64_t signrec = option(OPT_SIGNREC);
     // K1s (lcb_stream.cu), the warp-specialised streaming step: LCB_STREAM=0 keeps K1
     const int64_t stream_mode = option(OPT_STREAM);
-    const int sspan = 32 * static_cast<int>(16 / sizeof(T));  // one 512-byte slab
+    const int sspan = stream_slab_cols(static_cast<int>(sizeof(T)));  // one 1 KB slab
     const int nslabs = (W + sspan - 1) / sspan;
     // slab-outer order (all iterations of one slab before the next: members are independent,
     // ascent.cpp:52, so the slab's codes stay L2-resident across iterations) unless early exit
@@ -1054,8 +1055,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     // auto (-1): K1s where its slab-major order keeps the codes on chip (config 4); K1 where the
     // iterate itself is L2-resident (config 5: 166 vs 208 us/iteration for K1s)
     const bool use_stream = (stream_mode == 1 || (stream_mode < 0 && slab_outer)) && !trace_host &&
-                            step_span<T>(W) == sspan && w.ld % sspan == 0 &&
-                            static_cast<int64_t>(g.n) * 32 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
+                            w.ld % sspan == 0 &&
+                            static_cast<int64_t>(g.n) * 36 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
     static const int64_t l2_bytes = [] {
         int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, 0);
@@ -1065,11 +1066,13 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     const int span = step_span<T>(W);
     const bool codes_on = use_stream || signrec == 1 ||
                           (signrec != 0 && static_cast<int64_t>(g.n) * w.ld * static_cast<int64_t>(sizeof(T)) > l2_bytes);
-    if (codes_on && span == 32 * static_cast<int>(16 / sizeof(T)) && w.ld % span == 0) {
-        // K1: [n][sgn_ld] interleaved; K1s: [slabs][n][32] (one slab when slab-outer)
+    if (use_stream || (codes_on && span == 32 * static_cast<int>(16 / sizeof(T)) && w.ld % span == 0)) {
+        // K1: [n][sgn_ld] interleaved; K1s: [slabs][n][32] sign bytes + [slabs][n] u32 flags
+        // (one slab when slab-outer)
         a.sgn_ld = (w.ld / span) * 32;
-        const size_t bytes = use_stream ? static_cast<size_t>(g.n) * 32 * (slab_outer ? 1 : nslabs)
+        const size_t bytes = use_stream ? static_cast<size_t>(g.n) * 36 * (slab_outer ? 1 : nslabs)
                                         : static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld);
+        a.flag_off = static_cast<int64_t>(g.n) * 32 * (slab_outer ? 1 : nslabs);
         codes[0] = w.sgn.ensure(2 * bytes);
         codes[1] = codes[0] + bytes;
     }

@@ -1,24 +1,34 @@
-// lcb_stream.cu — K1s: warp-specialised streaming PGA step for graphs whose iterate
-// does not live on chip (configs 4 and 5; config 2's unlifted batches when K2 is off).
+// lcb_stream.cu — K1s: warp-specialised streaming PGA step for graphs whose iterate does
+// not live on chip (config 4: ER n=1M, W=512 -> 2 GB per iterate buffer).
 //
-// One launch = one iteration of ascent.cpp:58-77 over the whole batch (Jacobi: every
-// row reads the previous iterate of its neighbours).  Work unit = a tile of R rows x
-// one 512-byte column slab (128 fp32 / 64 fp64 columns).  Tiles are visited
-// slab-major by a persistent grid, so at any moment all SMs work on one slab and the
-// slab's saturation codes (1 byte per lane: 32 bytes per row; 32 MB for n = 1M) stay in
-// L2 while the iterate itself (2 GB for config 4) streams from HBM exactly once.
+// One launch = one iteration of ascent.cpp:58-77 (Jacobi: every row reads the previous
+// iterate of its neighbours) over the column slabs [slab0, slab0 + nslabs).  A slab is
+// 1 KB of a row: 256 fp32 / 128 fp64 columns.  Work unit = a tile of R consecutive rows x
+// one slab.  The runtime runs large batches slab-major (all iterations of one slab, then
+// the next: members are independent, ascent.cpp:52), so the slab's saturation codes stay
+// in L2 across iterations while the iterate itself streams from HBM once per iteration.
 //
-//   warp 0 (producer): per tile, the rows' CSR ranges, then cp.async.bulk copies of
-//           each row's x slab, v slab (512 B each, L2 evict-first) and its column
-//           list into a ring of stages, completion on an mbarrier;
-//   warps 1..R (consumers): one row of the tile each: neighbour sums from the codes
-//           (+-1 exactly) when a neighbour's lane elements sit on the box corners, else
-//           from the neighbour's x slab, in CSR order per element (graph.cpp:116-121,
-//           so fp64 stays bit-exact); fused heavy-ball / finite check / clamp
-//           (ascent.cpp:66-77); x', v' (evict-first) and the row's new code written
-//           straight from registers; then the stage is released.
-// The own-row traffic (x, v in; x', v' out) is the 16 B/node-update of the roofline
-// model; the gathers cost 32 B per neighbour and slab from L2 once saturated.
+//   warp 0 (producer): per tile one 2D TMA box of x and one of v ([R][1 KB], L2
+//           evict-first) and the tile's contiguous column run (bulk copy) into a ring of
+//           stages, completion on an mbarrier; the row_ptr range of the tile P ahead
+//           loads meanwhile.
+//   warps 1..R (consumers): one row of the tile each.  Lane l owns 8 fp32 (4 fp64)
+//           columns: the 16-byte groups l and 32+l of the slab (coalesced 512-byte
+//           halves).  The neighbours' 32-byte code lines (one sign byte per lane) and
+//           "row slab not saturated" flags of the NEXT tile's row are copied into the
+//           warp's SMEM buffer with cp.async while this row is processed.
+//
+// Neighbour sums, in CSR order per element (graph.cpp:116-121):
+//   * while every neighbour slab of a 32-neighbour batch is fully on the box corners (flag
+//     0), every partial sum is a small integer, exact in fp32 and fp64: the +1 counts are
+//     accumulated as SWAR bytes from the sign bits (sum = 2 * plus - count);
+//   * from the first batch with an interior neighbour the warp continues with sequential
+//     fp adds from that exact partial sum: +-1 from the sign bits for saturated
+//     neighbours, the neighbour's 32 bytes of x otherwise.
+// So fp64 stays bit-exact with the reference and fp32 equals the sequential fp32 sum.
+// Epilogue: fused heavy-ball / finite check / clamp (ascent.cpp:66-73; the shared
+// pga_raw op sequence, packed f32x2 FMAs), x' and v' written straight from registers
+// (evict-first), plus the row's new sign bytes and slab flag.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -44,35 +54,19 @@ constexpr int kThreadsS = 32 * (kR + 1);
 #define LCB_STREAM_STAGES 4
 #endif
 constexpr int kStages = LCB_STREAM_STAGES;
-constexpr int kColBuf = 32 * kR;  // int32 column slots per stage (aligned per-row runs)
-#ifndef LCB_STREAM_MINB
-#define LCB_STREAM_MINB 2
-#endif
-#ifndef LCB_STREAM_NB
-#define LCB_STREAM_NB 8
-#endif
-constexpr int kNB = LCB_STREAM_NB;  // neighbour codes in flight per batch
+constexpr int kColBuf = 32 * kR;  // int32 column slots per stage
 #ifndef LCB_STREAM_LOOK
 #define LCB_STREAM_LOOK 4
 #endif
 constexpr int kLook = LCB_STREAM_LOOK;  // producer lookahead (tiles) for the CSR ranges
+constexpr int kSlab = 1024;             // bytes of one row of a slab
 
 template <typename T>
-struct SVec;
-template <>
-struct SVec<float> {
-    using type = float4;
-    static constexpr int E = 4;
+struct Lanes {
+    static constexpr int E = kSlab / 32 / static_cast<int>(sizeof(T));  // elements per lane
+    static constexpr int H = E / 2;                                     // per 16-byte half
+    static constexpr int SPAN = 32 * E;                                 // columns per slab
 };
-template <>
-struct SVec<double> {
-    using type = double2;
-    static constexpr int E = 2;
-};
-__device__ __forceinline__ float& el(float4& v, int e) { return (&v.x)[e]; }
-__device__ __forceinline__ double& el(double2& v, int e) { return (&v.x)[e]; }
-__device__ __forceinline__ float el(const float4& v, int e) { return (&v.x)[e]; }
-__device__ __forceinline__ double el(const double2& v, int e) { return (&v.x)[e]; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -87,9 +81,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// the suspend-time hint parks a waiting warp in the barrier unit instead of re-issuing the probe
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    // the suspend-time hint parks the warp in the barrier unit instead of re-issuing the
-    // probe (waiting warps otherwise take issue slots from the working ones)
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -107,8 +100,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
-// 2D tensor tile (TMA): box [R rows][512 bytes] of X / V at (column c0, row r0); rows past
-// n are zero-filled and still counted in the transaction bytes
+// 2D tensor tile (TMA): box [R rows][1 KB] of X / V at (column c0, row r0); rows past n are
+// zero-filled and still counted in the transaction bytes
 __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* map, int c0, int r0, uint64_t* bar,
                                          uint64_t pol) {
     asm volatile(
@@ -122,98 +115,111 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// predicated code load (no branch): `fill` when !pred.  0xF0 = all four elements -1 is the
-// neutral filler of the integer path (saturated, no +1 counts)
-__device__ __forceinline__ uint32_t ld_code_if(const uint8_t* p, bool pred, uint32_t fill) {
-    uint32_t v;
-    asm volatile(
-        "{\n"
-        ".reg .pred q;\n"
-        "setp.ne.b32 q, %2, 0;\n"
-        "mov.b32 %0, %3;\n"
-        "@q ld.global.nc.L1::no_allocate.u8 %0, [%1];\n"
-        "}\n"
-        : "=r"(v)
-        : "l"(p), "r"(static_cast<uint32_t>(pred)), "r"(fill));
-    return v;
-}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ uint32_t lds_u8_if(const uint8_t* p, bool pred, uint32_t fill) {
-    uint32_t v;
-    asm volatile(
-        "{\n"
-        ".reg .pred q;\n"
-        "setp.ne.b32 q, %2, 0;\n"
-        "mov.b32 %0, %3;\n"
-        "@q ld.shared.u8 %0, [%1];\n"
-        "}\n"
-        : "=r"(v)
-        : "r"(smem_u32(p)), "r"(static_cast<uint32_t>(pred)), "r"(fill));
-    return v;
-}
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ float4 lds_v(const float4* p) {
-    float4 v;
+// 16-byte vectors of a lane's half-slab
+__device__ __forceinline__ void ld16(float* v, const void* smem) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(smem_u32(p)));
-    return v;
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "r"(smem_u32(smem)));
 }
-__device__ __forceinline__ double2 lds_v(const double2* p) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
-    return v;
+__device__ __forceinline__ void ld16(double* v, const void* smem) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(smem_u32(smem)));
 }
-__device__ __forceinline__ void stg_stream(float4* p, float4 v) { __stcs(p, v); }
-__device__ __forceinline__ void stg_stream(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void ldg16(float* v, const float* p) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+}
+__device__ __forceinline__ void ldg16(double* v, const double* p) {
+    const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = q.x;
+    v[1] = q.y;
+}
+__device__ __forceinline__ void stg16(float* p, const float* v) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void stg16(double* p, const double* v) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+}
 
 __device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
 
-// a neighbour slab whose lane elements are all on the box corners (+1 bit e / -1 bit 4+e)
-template <int E>
-__device__ __forceinline__ bool sat_code(uint32_t c) {
-    constexpr uint32_t full = (1u << E) - 1u;
-    return ((c | (c >> 4)) & full) == full;
+// packed fp32x2 FMA (FFMA2): round-to-nearest per lane, identical to two __fmaf_rn
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                     float c1) {
+    unsigned long long r;
+    const unsigned long long A = (static_cast<unsigned long long>(__float_as_uint(a1)) << 32) | __float_as_uint(a0);
+    const unsigned long long B = (static_cast<unsigned long long>(__float_as_uint(b1)) << 32) | __float_as_uint(b0);
+    const unsigned long long Cc = (static_cast<unsigned long long>(__float_as_uint(c1)) << 32) | __float_as_uint(c0);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(A), "l"(B), "l"(Cc));
+    d0 = __uint_as_float(static_cast<unsigned>(r));
+    d1 = __uint_as_float(static_cast<unsigned>(r >> 32));
+}
+// the pga_raw sequence (lcb_internal.h) for two elements at once: fp32 packed, fp64 scalar
+__device__ __forceinline__ void pga_raw2(const float* x, const float* ax, float* v, float alpha, float mu, float dg,
+                                         float* raw) {
+    float y0, y1;
+    fma2(y0, y1, dg, dg, x[0], x[1], -ax[0], -ax[1]);
+    fma2(v[0], v[1], mu, mu, v[0], v[1], y0, y1);
+    fma2(raw[0], raw[1], alpha, alpha, v[0], v[1], x[0], x[1]);
+}
+__device__ __forceinline__ void pga_raw2(const double* x, const double* ax, double* v, double alpha, double mu,
+                                         double dg, double* raw) {
+    raw[0] = pga_raw(x[0], ax[0], v[0], alpha, mu, dg);
+    raw[1] = pga_raw(x[1], ax[1], v[1], alpha, mu, dg);
+}
+// the same with the neighbour sum passed negated (nax = -Ax, exact): y = fma(dg, x, nax)
+__device__ __forceinline__ void pga_raw_neg2(const float* x, const float* nax, float* v, float alpha, float mu,
+                                             float dg, float* raw) {
+    float y0, y1;
+    fma2(y0, y1, dg, dg, x[0], x[1], nax[0], nax[1]);
+    fma2(v[0], v[1], mu, mu, v[0], v[1], y0, y1);
+    fma2(raw[0], raw[1], alpha, alpha, v[0], v[1], x[0], x[1]);
+}
+__device__ __forceinline__ void pga_raw_neg2(const double* x, const double* nax, double* v, double alpha, double mu,
+                                             double dg, double* raw) {
+    raw[0] = pga_raw(x[0], -nax[0], v[0], alpha, mu, dg);
+    raw[1] = pga_raw(x[1], -nax[1], v[1], alpha, mu, dg);
 }
 
-template <typename T>
 struct StreamSmem {
-    using V = typename SVec<T>::type;
-    V x[kStages][kR][32];
-    V v[kStages][kR][32];
+    unsigned char x[kStages][kR][kSlab];
+    unsigned char v[kStages][kR][kSlab];
     int col[kStages][kColBuf];
     int row[kStages][kR];
     int beg[kStages][kR];
     int deg[kStages][kR];
     int coff[kStages][kR];
-    int slab[kStages];             // launch-relative slab index of the tile in the stage
-    uint8_t codes[kR][2][32][32];  // per consumer warp: code lines of <= 32 neighbours, two rows
+    int slab[kStages];               // launch-relative slab of the tile in the stage
+    alignas(16) uint8_t codes[kR][2][32][32];  // per consumer warp: code lines of <= 32 neighbours, two rows
+    uint32_t flags[kR][2][32];       // and their "slab not saturated" flags
     uint64_t full[kStages];
     uint64_t empty[kStages];
 };
 
 template <typename T, bool GEN, bool EE>
-__global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<T> a, int rowtiles, int slab0, int nslabs,
-                                                                      const __grid_constant__ CUtensorMap mx,
-                                                                      const __grid_constant__ CUtensorMap mv) {
-    using V = typename SVec<T>::type;
-    constexpr int E = SVec<T>::E;
-    constexpr int SPAN = 32 * E;
+__global__ void __launch_bounds__(kThreadsS, 1)
+    k_stream(StepArgs<T> a, int rowtiles, int slab0, int nslabs, const __grid_constant__ CUtensorMap mx,
+             const __grid_constant__ CUtensorMap mv) {
+    constexpr int E = Lanes<T>::E, H = Lanes<T>::H, SPAN = Lanes<T>::SPAN;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    StreamSmem<T>& sm = *reinterpret_cast<StreamSmem<T>*>(smem_raw);
+    StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int ntiles = rowtiles * nslabs;
+    const uint32_t n32 = static_cast<uint32_t>(a.n);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -229,9 +235,8 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
     __syncthreads();
 
     if (warp == 0) {
-        // ---------------- producer.  Rows in natural order: a tile is R consecutive rows, so its
-        // x and v slabs are ONE 2D TMA box each ([R][512 B]) and its column lists one contiguous
-        // bulk copy.  The row_ptr range of tile i+P loads while tile i's copies are issued.
+        // ---------------- producer: this CTA's tiles t = blockIdx.x + i * gridDim.x, walked
+        // incrementally as (row tile, slab)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
@@ -239,11 +244,9 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
         const uint64_t pol = policy_evict_first();
         constexpr int P = kLook;
         int qrp[P];  // lane j <= R: row_ptr[min(r0 + j, n)] of the tile P ahead
-        // tile t = (row tile rt, slab sl); this CTA's tiles t = blockIdx.x + i * gridDim.x are
-        // walked incrementally (no division per tile)
         const int drt = static_cast<int>(gridDim.x) % rowtiles, dsl = static_cast<int>(gridDim.x) / rowtiles;
         int cur_rt = static_cast<int>(blockIdx.x) % rowtiles, cur_sl = static_cast<int>(blockIdx.x) / rowtiles;
-        int ah_rt = cur_rt, ah_sl = cur_sl;  // the tile P ahead
+        int ah_rt = cur_rt, ah_sl = cur_sl;
         auto adv = [&](int& rt, int& sl) {
             rt += drt;
             sl += dsl;
@@ -260,8 +263,6 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
         };
 #pragma unroll
         for (int q = 0; q < P; ++q) qrp[q] = fetch();
-        const CUtensorMap* mapx = &mx;
-        const CUtensorMap* mapv = &mv;
         for (int i0 = 0;; i0 += P) {
             bool done = false;
 #pragma unroll
@@ -281,10 +282,8 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
                 const int r0 = cur_rt * kR;
                 adv(cur_rt, cur_sl);
                 if (a.it & 1) sl = nslabs - 1 - sl;  // snake: reuse the slab just written
-                const int slab = slab0 + sl;
                 const int abeg = first & ~3;
-                const int need = ((last + 3) & ~3) - abeg;          // whole tile's column run
-                const int ncopy = min(need, kColBuf);                 // staged prefix
+                const int ncopy = min(((last + 3) & ~3) - abeg, kColBuf);  // staged prefix of the tile's run
                 if (lane == 0) sm.slab[s] = sl;
                 if (lane < kR) {
                     const int row = r0 + lane;
@@ -296,10 +295,9 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    const uint32_t bytes = 2u * kR * 512u + static_cast<uint32_t>(ncopy) * 4u;
-                    mbar_expect_tx(&sm.full[s], bytes);
-                    tma_tile(&sm.x[s][0][0], mapx, slab * SPAN, r0, &sm.full[s], pol);
-                    tma_tile(&sm.v[s][0][0], mapv, slab * SPAN, r0, &sm.full[s], pol);
+                    mbar_expect_tx(&sm.full[s], 2u * kR * kSlab + static_cast<uint32_t>(ncopy) * 4u);
+                    tma_tile(&sm.x[s][0][0], &mx, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
+                    tma_tile(&sm.v[s][0][0], &mv, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
                     if (ncopy > 0)
                         bulk_g2s(&sm.col[s][0], a.col + abeg, static_cast<uint32_t>(ncopy) * 4u, &sm.full[s], pol);
                 }
@@ -311,15 +309,13 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
 
     // ---------------- consumers: warp w owns row w-1 of every tile
     const int j = warp - 1;
-    const uint64_t pol_keep = policy_evict_last();
-    constexpr uint32_t FULL = (1u << E) - 1u;
-    // per-slab lane state, fixed for the whole launch (no per-row division / loads): which of
-    // the lane's elements step at this iteration (bit e), the member of element e is
-    // recomputed only on the rare paths that need it (exit bits, non-finite values)
+    // lane element e: half e / H (16-byte group lane or 32 + lane of the slab), position e % H
+    auto col_of = [&](int slab, int e) { return slab * SPAN + (e / H) * (SPAN / 2) + lane * H + (e % H); };
+    auto member_of = [&](int slab, int e) { return (a.col_base + col_of(slab, e)) / a.l; };
     int cur_slab = -1;
-    uint32_t act_bits = 0;
-    uint32_t ebits = 0;  // 3 exit bits per element (EE)
-    auto member_of = [&](int slab, int e) { return (a.col_base + slab * SPAN + lane * E + e) / a.l; };
+    uint32_t act_bits = 0;  // which elements step at this iteration (bit e)
+    bool all_act = false;
+    uint32_t ebits = 0;     // 3 exit bits per element (EE)
     auto flush_bits = [&]() {
         if constexpr (EE) {
 #pragma unroll
@@ -340,8 +336,7 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
         act_bits = 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int colx = slab * SPAN + lane * E + e;
-            bool act = colx < a.W;
+            bool act = col_of(slab, e) < a.W;
             if constexpr (GEN) {
                 if (act) {
                     const int m = member_of(slab, e);
@@ -353,30 +348,26 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
             }
             act_bits |= act ? 1u << e : 0u;
         }
+        all_act = __all_sync(0xffffffffu, act_bits == (1u << E) - 1u);
     };
-    bool float_hint = false;  // the previous row met an unsaturated neighbour
+    const uint8_t* const cin = a.sgn_in;  // codes [slabs][n][32], flags [slabs][n] at flag_off
+    const uint32_t* const fin = cin ? reinterpret_cast<const uint32_t*>(cin + a.flag_off) : nullptr;
+    uint8_t* const cout = a.sgn_out;
+    uint32_t* const fout = cout ? reinterpret_cast<uint32_t*>(cout + a.flag_off) : nullptr;
 
-    // The code lines (32 B) of a row's first <= 32 neighbours are copied into this warp's
-    // SMEM buffer with cp.async one tile ahead (lane k copies neighbour k), so the
-    // neighbour sums read SMEM only and the L2 latency of the gathers is off the critical path.
-    auto issue_codes = [&](int st, int sl, int buf) {
+    // code lines + flags of neighbours [k0, k0 + 32) of the row in stage st -> buffer buf
+    auto stage_codes = [&](int st, int sl, int buf, int k0) {
         const int row = sm.row[st][j];
-        if (row >= 0 && a.sgn_in) {
+        if (row >= 0 && cin) {
             const int deg = sm.deg[st][j];
-            uint8_t* dst = &sm.codes[j][buf][lane][0];
-            if (lane < deg) {
+            const int k = k0 + lane;
+            if (k < deg) {
                 const int coff = sm.coff[st][j];
-                const int u = coff >= 0 ? sm.col[st][coff + lane] : __ldg(a.col + sm.beg[st][j] + lane);
-                const uint8_t* src =
-                    a.sgn_in + (static_cast<uint32_t>(sl) * static_cast<uint32_t>(a.n) + static_cast<uint32_t>(u)) * 32u;
-                cp_async16(dst, src);
-                cp_async16(dst + 16, src + 16);
-            } else if (lane < ((deg + 3) & ~3)) {
-                // neutral filler up to a multiple of 4: every element -1 (saturated, no +1 count),
-                // so the integer loop runs without bounds checks
-                const uint4 f = make_uint4(0xF0F0F0F0u, 0xF0F0F0F0u, 0xF0F0F0F0u, 0xF0F0F0F0u);
-                reinterpret_cast<uint4*>(dst)[0] = f;
-                reinterpret_cast<uint4*>(dst)[1] = f;
+                const int u = coff >= 0 ? sm.col[st][coff + k] : __ldg(a.col + sm.beg[st][j] + k);
+                const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(u);
+                cp_async16(&sm.codes[j][buf][lane][0], cin + line * 32u);
+                cp_async16(&sm.codes[j][buf][lane][16], cin + line * 32u + 16u);
+                cp_async4(&sm.flags[j][buf][lane], fin + line);
             }
         }
         cp_async_commit();
@@ -386,18 +377,18 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
                          static_cast<int>(gridDim.x);
     if (my_tiles > 0) {
         mbar_wait(&sm.full[0], 0);
-        issue_codes(0, sm.slab[0], 0);
+        stage_codes(0, sm.slab[0], 0, 0);
     }
+    bool float_hint = false;  // the previous row met an interior neighbour: start in fp mode
     for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
         const int sl = sm.slab[s];
         const int slab = slab0 + sl;
         if (slab != cur_slab) enter_slab(slab);
-        // next tile: its stage is normally landed already (the producer runs ahead)
-        if (i + 1 < my_tiles) {
+        if (i + 1 < my_tiles) {  // the next tile's stage has normally landed (the producer runs ahead)
             const int sn = (i + 1) % kStages;
             mbar_wait(&sm.full[sn], ((i + 1) / kStages) & 1);
-            issue_codes(sn, sm.slab[sn], (i + 1) & 1);
+            stage_codes(sn, sm.slab[sn], (i + 1) & 1, 0);
         } else {
             cp_async_commit();
         }
@@ -407,127 +398,158 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
         if (row >= 0) {
             const int deg = sm.deg[s][j];
             const int coff = sm.coff[s][j];
-            const int* cl = coff >= 0 ? &sm.col[s][coff] : a.col + sm.beg[s][j];
-            const int c0 = slab * SPAN + lane * E;
-            const uint8_t* cb = &sm.codes[j][i & 1][0][lane];  // neighbour k's byte for this lane: cb[32 k]
-            // codes of this launch's slab sl beyond the staged 32 neighbours: [nslabs][n][32] (< 4 GB)
-            const uint8_t* sin =
-                a.sgn_in ? a.sgn_in + static_cast<uint32_t>(sl) * static_cast<uint32_t>(a.n) * 32u + lane : nullptr;
-            // Neighbour sums in CSR order (graph.cpp:116-121).  While every neighbour element of
-            // the lane sits on a box corner the partial sums are small integers, exact in fp32 /
-            // fp64, so they are kept as integer counts of +1 (SWAR bytes: code bit e -> byte e);
-            // from the first batch with an interior value on ANY lane the warp continues with
-            // sequential fp adds starting from that exact partial sum.
-            uint32_t pe[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) pe[e] = 0;
-            int folded = 0;
-            bool fmode = sin == nullptr || float_hint;
-            V acc;
-#pragma unroll
-            for (int e = 0; e < E; ++e) el(acc, e) = T(0);
+            const int buf = i & 1;
+            const uint8_t* cb = &sm.codes[j][buf][0][lane];  // neighbour k's sign byte for this lane: cb[32 k]
+            const uint32_t* fb = &sm.flags[j][buf][0];
+            const T* xin0 = a.x_in + col_of(slab, 0);
+            const T* xin1 = xin0 + SPAN / 2;
+            // integer mode: SWAR byte counters of +1 signs, p0 elements 0..3, p1 elements 4..7
+            // (<= 224 neighbours per fold; hub rows fold into wide counters)
+            uint32_t p0 = 0, p1 = 0, wide[E];
+            int folded = 0, in_bytes = 0;
+            bool wide_used = false;
+            bool fmode = cin == nullptr || float_hint;
+            T acc[E];  // fp mode: the running sum
+            auto unpack = [&](int e) -> uint32_t {
+                return __byte_perm(e < 4 ? p0 : p1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
+            };
             for (int base = 0; base < deg; base += 32) {
                 const int cnt = min(32, deg - base);
-                const bool staged = base == 0;
-                int mycol = 0;  // neighbour index of this lane's slot (global path / float path only)
-                if (!staged) mycol = lane < cnt ? cl[base + lane] : 0;
+                if (base > 0 && cin) {  // hub rows: the next 32 neighbours, staged synchronously
+                    __syncwarp();
+                    stage_codes(s, sl, buf, base);
+                    cp_async_wait0();
+                    __syncwarp();
+                }
                 if (!fmode) {
-                    uint32_t A = 0xFFu, plus = 0;
-                    if (staged) {
-                        for (int k = 0; k < cnt; k += 4) {  // lines cnt..round4(cnt) hold the filler
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint32_t c = cb[32 * (k + q)];
-                                A &= c | (c >> 4);
-                                plus += ((c & 0xFu) * 0x00204081u) & 0x01010101u;  // bit e -> byte e, no carries
-                            }
+                    const bool interior = __any_sync(0xffffffffu, lane < cnt && fb[lane] != 0u);
+                    if (!interior) {
+#pragma unroll 4
+                        for (int k = 0; k < cnt; ++k) {
+                            const uint32_t b = cb[32 * k];
+                            p0 += ((b & 0xFu) * 0x00204081u) & 0x01010101u;  // sign bit e -> byte e
+                            if constexpr (E == 8) p1 += ((b >> 4) * 0x00204081u) & 0x01010101u;
                         }
-                    } else {
-                        for (int k = 0; k < cnt; k += kNB) {
-                            uint32_t cq[kNB];
-#pragma unroll
-                            for (int q = 0; q < kNB; ++q) {
-                                const uint32_t u = static_cast<uint32_t>(__shfl_sync(0xffffffffu, mycol, (k + q) & 31));
-                                cq[q] = ld_code_if(sin + u * 32u, k + q < cnt, 0xF0u);
-                            }
-#pragma unroll
-                            for (int q = 0; q < kNB; ++q) {
-                                A &= cq[q] | (cq[q] >> 4);
-                                plus += ((cq[q] & 0xFu) * 0x00204081u) & 0x01010101u;
-                            }
-                        }
-                    }
-                    if (__all_sync(0xffffffffu, (A & FULL) == FULL)) {
-#pragma unroll
-                        for (int e = 0; e < E; ++e) pe[e] += (plus >> (8 * e)) & 0xFFu;
                         folded += cnt;
+                        in_bytes += cnt;
+                        if (in_bytes > 224) {  // hub rows: keep the byte counters from overflowing
+                            if (!wide_used) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e) wide[e] = 0;
+                                wide_used = true;
+                            }
+#pragma unroll
+                            for (int e = 0; e < E; ++e) wide[e] += unpack(e);
+                            p0 = p1 = 0;
+                            in_bytes = 0;
+                        }
                         continue;
                     }
                     fmode = true;  // exact partial sum so far: (+1 count) - (-1 count)
 #pragma unroll
-                    for (int e = 0; e < E; ++e) el(acc, e) = static_cast<T>(2 * static_cast<int>(pe[e]) - folded);
-                }
-                if (staged) mycol = lane < cnt ? cl[base + lane] : 0;
-                const T* xin = a.x_in + c0;
-                for (int k = 0; k < cnt; k += 4) {
-                    uint32_t cq[4];
-                    V g[4];
+                    for (int e = 0; e < E; ++e)
+                        acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
+                } else if (base == 0) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int u = __shfl_sync(0xffffffffu, mycol, (k + q) & 31);
-                        const bool in = sin != nullptr && k + q < cnt;
-                        cq[q] = staged ? lds_u8_if(cb + 32 * ((k + q) & 31), in, 0u)
-                                       : ld_code_if(sin + static_cast<uint32_t>(u) * 32u, in, 0u);
-                        if (k + q < cnt && !sat_code<E>(cq[q]))
-                            g[q] = __ldg(reinterpret_cast<const V*>(xin + static_cast<int64_t>(u) * a.ld));
+                    for (int e = 0; e < E; ++e) acc[e] = T(0);
+                }
+                // sequential fp adds; the neighbour index is only needed for interior neighbours
+                for (int k = 0; k < cnt; k += 2) {
+                    T g[2][E];
+                    uint32_t bq[2];
+                    bool in[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int kk = k + q;
+                        const bool live = kk < cnt;
+                        in[q] = live && (cin == nullptr || fb[kk] != 0u);  // warp-uniform
+                        bq[q] = (live && cin) ? cb[32 * kk] : 0u;
+                        if (in[q]) {
+                            const int u =
+                                coff >= 0 ? sm.col[s][coff + base + kk] : __ldg(a.col + sm.beg[s][j] + base + kk);
+                            const int64_t o = static_cast<int64_t>(u) * a.ld;
+                            ldg16(&g[q][0], xin0 + o);
+                            ldg16(&g[q][H], xin1 + o);
+                        }
                     }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
+                    for (int q = 0; q < 2; ++q) {
                         if (k + q < cnt) {
-                            const bool sat = sat_code<E>(cq[q]);
 #pragma unroll
                             for (int e = 0; e < E; ++e)
-                                el(acc, e) = radd(el(acc, e), sat ? (((cq[q] >> e) & 1u) ? T(1) : T(-1)) : el(g[q], e));
+                                acc[e] = radd(acc[e], in[q] ? g[q][e] : (((bq[q] >> e) & 1u) ? T(1) : T(-1)));
                         }
                     }
                 }
             }
+            // -acc, exact: -((count of +1) - (count of -1)); negated after the conversion so a zero
+            // sum is -0.0 exactly as -(+0.0) of the sequential sum
+            T nacc[E];
             if (!fmode) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) el(acc, e) = static_cast<T>(2 * static_cast<int>(pe[e]) - folded);
-            }
-            float_hint = fmode && sin != nullptr;
-
-            const V xv = lds_v(&sm.x[s][j][lane]);
-            V vv = lds_v(&sm.v[s][j][lane]);
-            const T dg = static_cast<T>(deg);
-            V xo;
-            uint32_t code = 0, bad = 0;
+                for (int e = 0; e < E; ++e)
+                    nacc[e] = -static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
+            } else {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const T x = el(xv, e);
-                const bool act = (act_bits >> e) & 1u;
-                T alpha = a.alpha_uniform;
-                if constexpr (GEN) {
-                    if (a.alpha) alpha = __ldg(a.alpha + member_of(slab, e));
+                for (int e = 0; e < E; ++e) nacc[e] = -acc[e];
+            }
+            float_hint = fmode && cin != nullptr;
+
+            // ---- epilogue (ascent.cpp:66-77)
+            T xv[E], vv[E];
+            ld16(&xv[0], &sm.x[s][j][16 * lane]);
+            ld16(&xv[H], &sm.x[s][j][512 + 16 * lane]);
+            ld16(&vv[0], &sm.v[s][j][16 * lane]);
+            ld16(&vv[H], &sm.v[s][j][512 + 16 * lane]);
+            const T dg = static_cast<T>(deg);
+            T raw[E], xo[E];
+            uint32_t bad = 0, sign = 0;
+            bool interior = false;
+            if (all_act && !(GEN && a.alpha)) {
+                // every element steps with the uniform alpha (the steady state)
+#pragma unroll
+                for (int e = 0; e < E; e += 2) pga_raw_neg2(&xv[e], &nacc[e], &vv[e], a.alpha_uniform, a.mu, dg, &raw[e]);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    bad |= isfinite(raw[e]) ? 0u : 1u << e;                  // ascent.cpp:70-72
+                    xo[e] = fmin(fmax(raw[e], T(-1)), T(1));                 // ascent.cpp:73 (raw finite)
+                    if constexpr (EE) {
+                        const T ch = fabs(xo[e] - xv[e]);
+                        uint32_t b = 0;
+                        if (ch > T(1e-12)) b |= EX_BIG;
+                        if (ch > T(0)) b |= EX_NZ;
+                        if (xo[e] != T(1) && xo[e] != T(-1)) b |= EX_NOTB;
+                        ebits |= b << (3 * e);
+                    }
+                    sign |= (xo[e] > T(0) ? 1u : 0u) << e;
+                    interior |= fabs(xo[e]) != T(1);
                 }
-                T vel = el(vv, e);
-                const T raw = pga_raw(x, el(acc, e), vel, alpha, a.mu, dg);
-                bad |= (act && !isfinite(raw)) ? 1u << e : 0u;       // ascent.cpp:70-72
-                const T cl = fmin(fmax(raw, T(-1)), T(1));             // ascent.cpp:73 (raw finite)
-                const T o = act ? cl : x;
-                if constexpr (EE) {
-                    const T ch = fabs(cl - x);
-                    uint32_t b = 0;
-                    if (ch > T(1e-12)) b |= EX_BIG;
-                    if (ch > T(0)) b |= EX_NZ;
-                    if (cl != T(1) && cl != T(-1)) b |= EX_NOTB;
-                    ebits |= (act ? b : 0u) << (3 * e);
+            } else {
+                T vn[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    vn[e] = vv[e];
+                    const T alpha = (GEN && a.alpha) ? __ldg(a.alpha + member_of(slab, e)) : a.alpha_uniform;
+                    raw[e] = pga_raw(xv[e], -nacc[e], vn[e], alpha, a.mu, dg);
                 }
-                el(vv, e) = act ? vel : el(vv, e);
-                el(xo, e) = o;
-                code |= (o == T(1) ? 1u : 0u) << e;
-                code |= (o == T(-1) ? 16u : 0u) << e;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool act = (act_bits >> e) & 1u;
+                    bad |= (act && !isfinite(raw[e])) ? 1u << e : 0u;
+                    const T cl = fmin(fmax(raw[e], T(-1)), T(1));
+                    if constexpr (EE) {
+                        const T ch = fabs(cl - xv[e]);
+                        uint32_t b = 0;
+                        if (ch > T(1e-12)) b |= EX_BIG;
+                        if (ch > T(0)) b |= EX_NZ;
+                        if (cl != T(1) && cl != T(-1)) b |= EX_NOTB;
+                        ebits |= (act ? b : 0u) << (3 * e);
+                    }
+                    xo[e] = act ? cl : xv[e];
+                    vv[e] = act ? vn[e] : vv[e];
+                    sign |= (xo[e] > T(0) ? 1u : 0u) << e;
+                    interior |= fabs(xo[e]) != T(1);
+                }
             }
             if (bad) {
 #pragma unroll
@@ -538,12 +560,18 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB) k_stream(StepArgs<
                                   (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(a.it));
                     }
             }
-            const int64_t off = static_cast<int64_t>(row) * a.ld + c0;
-            stg_stream(reinterpret_cast<V*>(a.x_out + off), xo);
-            stg_stream(reinterpret_cast<V*>(a.vel + off), vv);
-            if (a.sgn_out)
-                a.sgn_out[(static_cast<uint32_t>(sl) * static_cast<uint32_t>(a.n) + static_cast<uint32_t>(row)) * 32u + lane] =
-                    static_cast<uint8_t>(code);
+            T* xo0 = a.x_out + static_cast<int64_t>(row) * a.ld + col_of(slab, 0);
+            T* vo0 = a.vel + static_cast<int64_t>(row) * a.ld + col_of(slab, 0);
+            stg16(xo0, &xo[0]);
+            stg16(xo0 + SPAN / 2, &xo[H]);
+            stg16(vo0, &vv[0]);
+            stg16(vo0 + SPAN / 2, &vv[H]);
+            if (cout) {
+                const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(row);
+                cout[line * 32u + lane] = static_cast<uint8_t>(sign);
+                const bool any_interior = __any_sync(0xffffffffu, interior);
+                if (lane == 0) fout[line] = any_interior ? 1u : 0u;
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -567,25 +595,26 @@ EncodeTiledFn tiled_encoder() {
     return fn;
 }
 
-// X / V [n][ld] as a 2D tensor; box = one 512-byte slab of R rows, no swizzle (the SMEM
-// stage is [R][512 B] row-major, as the consumers read it)
+// X / V [n][ld] as a 2D tensor; box = one 1 KB slab row x R rows, no swizzle (the SMEM
+// stage is [R][1 KB] row-major, as the consumers read it)
 void slab_map(CUtensorMap* m, const void* base, int64_t ld, int n, int elem_bytes) {
     EncodeTiledFn enc = tiled_encoder();
     if (!enc) throw Failure{LCB_CUDA, "cuTensorMapEncodeTiled unavailable"};
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(n)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * static_cast<cuuint64_t>(elem_bytes)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(512 / elem_bytes), static_cast<cuuint32_t>(kR)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kSlab / elem_bytes), static_cast<cuuint32_t>(kR)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = enc(m, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Failure{LCB_CUDA, "cuTensorMapEncodeTiled(slab) failed: " + std::to_string(static_cast<int>(r))};
+    if (r != CUDA_SUCCESS)
+        throw Failure{LCB_CUDA, "cuTensorMapEncodeTiled(slab) failed: " + std::to_string(static_cast<int>(r))};
 }
 
 template <typename T, bool GEN, bool EE>
 void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
-    const int smem = static_cast<int>(sizeof(StreamSmem<T>));
+    const int smem = static_cast<int>(sizeof(StreamSmem));
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     ensure_smem_attr(reinterpret_cast<const void*>(k_stream<T, GEN, EE>), smem, "cudaFuncSetAttribute(k_stream)");
@@ -610,6 +639,8 @@ void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
 }
 
 }  // namespace
+
+int stream_slab_cols(int elem_bytes) { return kSlab / elem_bytes; }
 
 template <typename T>
 void launch_stream(const StepArgs<T>& a, int slab0, int nslabs, bool early_exit, cudaStream_t s) {

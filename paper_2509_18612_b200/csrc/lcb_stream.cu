@@ -60,6 +60,10 @@ constexpr int kColBuf = 32 * kR;  // int32 column slots per stage
 #endif
 constexpr int kLook = LCB_STREAM_LOOK;  // producer lookahead (tiles) for the CSR ranges
 constexpr int kSlab = 1024;             // bytes of one row of a slab
+#ifndef LCB_STREAM_FNB
+#define LCB_STREAM_FNB 2
+#endif
+constexpr int kFNB = LCB_STREAM_FNB;    // interior-neighbour gathers in flight (fp mode)
 
 template <typename T>
 struct Lanes {
@@ -379,7 +383,6 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         mbar_wait(&sm.full[0], 0);
         stage_codes(0, sm.slab[0], 0, 0);
     }
-    bool float_hint = false;  // the previous row met an interior neighbour: start in fp mode
     for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
         const int sl = sm.slab[s];
@@ -408,8 +411,10 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             uint32_t p0 = 0, p1 = 0, wide[E];
             int folded = 0, in_bytes = 0;
             bool wide_used = false;
-            bool fmode = cin == nullptr || float_hint;
+            bool fmode = cin == nullptr;
             T acc[E];  // fp mode: the running sum
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = T(0);
             auto unpack = [&](int e) -> uint32_t {
                 return __byte_perm(e < 4 ? p0 : p1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
             };
@@ -449,17 +454,14 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 #pragma unroll
                     for (int e = 0; e < E; ++e)
                         acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
-                } else if (base == 0) {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) acc[e] = T(0);
                 }
                 // sequential fp adds; the neighbour index is only needed for interior neighbours
-                for (int k = 0; k < cnt; k += 2) {
-                    T g[2][E];
-                    uint32_t bq[2];
-                    bool in[2];
+                for (int k = 0; k < cnt; k += kFNB) {
+                    T g[kFNB][E];
+                    uint32_t bq[kFNB];
+                    bool in[kFNB];
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
+                    for (int q = 0; q < kFNB; ++q) {
                         const int kk = k + q;
                         const bool live = kk < cnt;
                         in[q] = live && (cin == nullptr || fb[kk] != 0u);  // warp-uniform
@@ -472,8 +474,19 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                             ldg16(&g[q][H], xin1 + o);
                         }
                     }
+                    bool all_in = true;
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
+                    for (int q = 0; q < kFNB; ++q) all_in = all_in && (in[q] || k + q >= cnt);
+                    if (all_in) {  // before saturation: every neighbour gathered, plain adds
+#pragma unroll
+                        for (int q = 0; q < kFNB; ++q)
+                            if (k + q < cnt)
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[e] = radd(acc[e], g[q][e]);
+                        continue;
+                    }
+#pragma unroll
+                    for (int q = 0; q < kFNB; ++q) {
                         if (k + q < cnt) {
 #pragma unroll
                             for (int e = 0; e < E; ++e)
@@ -493,7 +506,6 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 #pragma unroll
                 for (int e = 0; e < E; ++e) nacc[e] = -acc[e];
             }
-            float_hint = fmode && cin != nullptr;
 
             // ---- epilogue (ascent.cpp:66-77)
             T xv[E], vv[E];

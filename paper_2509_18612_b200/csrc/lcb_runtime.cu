@@ -75,7 +75,7 @@ struct OptDef {
     int64_t def;
 };
 constexpr OptDef kOptDefs[OPT_COUNT] = {
-    {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", -1},        {"signrec", "LCB_SIGNREC", -1},
+    {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", 1},         {"signrec", "LCB_SIGNREC", -1},
     {"chunk", "LCB_CHUNK", 0},        {"res_split", "LCB_RES_SPLIT", 1},   {"bank_order", "LCB_BANK_ORDER", 2},
     {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1}, {"slab_outer", "LCB_SLAB_OUTER", -1},
 };
@@ -1052,8 +1052,8 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
     const int64_t so = option(OPT_SLAB_OUTER);
     const bool slab_outer = (!ee || sspan % l == 0) && nslabs > 1 &&
                             (so == 1 || (so < 0 && static_cast<int64_t>(g.n) * 32 * nslabs * 2 > l2b / 2));
-    // auto (-1): K1s where its slab-major order keeps the codes on chip (config 4); K1 where the
-    // iterate itself is L2-resident (config 5: 166 vs 208 us/iteration for K1s)
+    // default 1: K1s for every streaming step (config 4: 1.83 vs 3.6 ms/iteration, config 5:
+    // 148 vs 166 us); -1: K1s only where the slab-major order is needed
     const bool use_stream = (stream_mode == 1 || (stream_mode < 0 && slab_outer)) && !trace_host &&
                             w.ld % sspan == 0 &&
                             static_cast<int64_t>(g.n) * 36 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
@@ -1070,8 +1070,9 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         // K1: [n][sgn_ld] interleaved; K1s: [slabs][n][32] sign bytes + [slabs][n] u32 flags
         // (one slab when slab-outer)
         a.sgn_ld = (w.ld / span) * 32;
-        const size_t bytes = use_stream ? static_cast<size_t>(g.n) * 36 * (slab_outer ? 1 : nslabs)
-                                        : static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld);
+        // second buffer 256-byte aligned (K1s copies 16-byte code lines with cp.async)
+        const size_t bytes = ((use_stream ? static_cast<size_t>(g.n) * 36 * (slab_outer ? 1 : nslabs)
+                                          : static_cast<size_t>(g.n) * static_cast<size_t>(a.sgn_ld)) + 255) & ~size_t(255);
         a.flag_off = static_cast<int64_t>(g.n) * 32 * (slab_outer ? 1 : nslabs);
         codes[0] = w.sgn.ensure(2 * bytes);
         codes[1] = codes[0] + bytes;

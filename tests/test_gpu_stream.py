@@ -80,6 +80,25 @@ def test_stream_fp64_low_skew_natural_order_and_isolated_rows():
         assert np.array_equal(run(pg(cg), x, n, 1, B, 0.05, 50, 0.9, ee, LCB_FP64), want), ee
 
 
+@pytest.mark.parametrize("prec", [LCB_FP64, LCB_FP32])
+@pytest.mark.parametrize("l,B,ee", [(2, 32, False), (2, 32, True), (1, 70, False)])
+def test_stream_small_graph_single_partial_slab(prec, l, B, ee):
+    """n = 250 (code buffers whose size is not a multiple of 16 bytes), one partial slab."""
+    cg = O.generate_er(250, 0.05, 9)
+    rng = np.random.default_rng(l + B)
+    x = rng.normal(0, 1e-4, B * l * cg.n)
+    want, _ = O.ascend(cg, x, l, B, 0.05, 60, 0.9, ee)
+    got = run(pg(cg), x, cg.n, l, B, 0.05, 60, 0.9, ee, prec)
+    if prec == LCB_FP64:
+        assert np.array_equal(got, want)
+    else:  # the same CSR-order sums and epilogue as K1: bit for bit
+        s = lc.DenseState(cg.n, l, B)
+        s.values[:] = x
+        with lc.options(resident=0, stream=0, chunk=0):
+            lc.ascend(pg(cg), s, lc.AscentParams(0.05, 60, 0.9, ee), precision=prec)
+        assert np.array_equal(got, s.values)
+
+
 def test_stream_fp64_hub_beyond_staged_columns():
     # one row with 3000 neighbours: its column list does not fit the stage buffer and is
     # read from global memory; a second hub row in the same tile

@@ -123,6 +123,10 @@ int lcb_lifted_init_mean(const lcb_graph* g, int32_t method, double beta, int32_
                          uint64_t key, double* mean);
 int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, double eta,
                        int64_t B, uint64_t key, double* out);
+/* gaussian_batch bit-identical to the reference (init.cpp:69-87: host libm Box-Muller on
+ * the member streams, members on host threads) -- the seeding the fp64 mode uses. */
+int lcb_gaussian_batch_exact(const double* mean, int64_t n, int32_t l, double eta, int64_t B,
+                             uint64_t key, double* out);
 
 /* ---- solver (solver.hpp:26-90) ---------------------------------------------- */
 typedef struct lcb_config { /* SolverConfig + AscentParams + InitConfig + SearchConfig */

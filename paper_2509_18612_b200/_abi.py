@@ -87,6 +87,7 @@ SIGNATURES = {
     "lcb_idi_init": (C.c_int, [P, f64, u64, P]),
     "lcb_lifted_init_mean": (C.c_int, [P, i32, f64, i32, u64, P]),
     "lcb_gaussian_batch": (C.c_int, [C.c_int, P, i64, i32, f64, i64, u64, P]),
+    "lcb_gaussian_batch_exact": (C.c_int, [P, i64, i32, f64, i64, u64, P]),
     "lcb_solve": (C.c_int, [P, P, u64, i32, P, P, P, P, i64, P, i64, P, i64]),
     "lcb_comm_unique_id": (C.c_int, [P]),
     "lcb_comm_create": (C.c_int, [P, i32, i32, C.c_int, C.POINTER(P)]),

@@ -2399,6 +2399,38 @@ int lcb_gaussian_batch(int device, const double* mean, int64_t n, int32_t l, dou
     });
 }
 
+int lcb_gaussian_batch_exact(const double* mean, int64_t n, int32_t l, double eta, int64_t B, uint64_t key,
+                             double* out) {
+    return guard([&] {
+        if (eta <= 0.0) fail(LCB_VALIDATION, "gaussian_batch: eta must be > 0");
+        if (n < 1 || l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+        if (!mean || !out) fail(LCB_VALIDATION, "null argument");
+        // the stream seeding of init.cpp:69-87 (member j: split(key, {0x6d62, j}), counters 2k,
+        // 2k+1 Box-Muller with the host libm), members on host threads; bit-identical
+        const size_t entries = static_cast<size_t>(n) * static_cast<size_t>(l);
+        const double noise = std::sqrt(eta);
+        auto gen = [&](int64_t j0, int64_t j1) {
+            for (int64_t j = j0; j < j1; ++j) {
+                HostStream ms{split2(key, 0x6d62u, static_cast<uint64_t>(j))};
+                double* o = out + static_cast<size_t>(j) * entries;
+                for (size_t k = 0; k < entries; ++k) {
+                    const double x = mean[k] + noise * ms.normal();
+                    o[k] = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+                }
+            }
+        };
+        const int64_t nt = std::min<int64_t>(B, std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+        if (nt <= 1 || entries * static_cast<size_t>(B) < (1u << 16)) {
+            gen(0, B);
+            return;
+        }
+        std::vector<std::thread> th;
+        for (int64_t t = 1; t < nt; ++t) th.emplace_back(gen, B * t / nt, B * (t + 1) / nt);
+        gen(0, B / nt);
+        for (auto& t : th) t.join();
+    });
+}
+
 int lcb_solve(const lcb_graph* g, const lcb_config* cfg, uint64_t seed, int32_t per_component,
               const lcb_run_opts* opts, lcb_outcome* out, uint8_t* assignment, lcb_batch_trace* bt,
               int64_t bt_cap, lcb_phase_trace* pt, int64_t pt_cap, lcb_search_trace* st, int64_t st_cap) {

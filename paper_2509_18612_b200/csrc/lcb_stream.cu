@@ -207,8 +207,10 @@ struct StreamSmem {
     int deg[kStages][kR];
     int coff[kStages][kR];
     int slab[kStages];               // launch-relative slab of the tile in the stage
-    alignas(16) uint8_t codes[kR][2][32][32];  // per consumer warp: code lines of <= 32 neighbours, two rows
-    uint32_t flags[kR][2][32];       // and their "slab not saturated" flags
+    // per consumer warp: code lines of <= 32 neighbours (this row, the next tile's row, and a
+    // third buffer that double-buffers the further 32-neighbour chunks of hub rows)
+    alignas(16) uint8_t codes[kR][3][32][32];
+    uint32_t flags[kR][3][32];       // and their "slab not saturated" flags
     uint64_t full[kStages];
     uint64_t empty[kStages];
 };
@@ -402,8 +404,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             const int deg = sm.deg[s][j];
             const int coff = sm.coff[s][j];
             const int buf = i & 1;
-            const uint8_t* cb = &sm.codes[j][buf][0][lane];  // neighbour k's sign byte for this lane: cb[32 k]
-            const uint32_t* fb = &sm.flags[j][buf][0];
+            int cur = buf;  // buffer holding the current 32-neighbour chunk
             const T* xin0 = a.x_in + col_of(slab, 0);
             const T* xin1 = xin0 + SPAN / 2;
             // integer mode: SWAR byte counters of +1 signs, p0 elements 0..3, p1 elements 4..7
@@ -420,12 +421,20 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             };
             for (int base = 0; base < deg; base += 32) {
                 const int cnt = min(32, deg - base);
-                if (base > 0 && cin) {  // hub rows: the next 32 neighbours, staged synchronously
+                int nxt = cur;
+                if (cin && base + 32 < deg) {  // hub rows: stage the next chunk while this one is summed
+                    nxt = cur == 2 ? buf : 2;
+                    __syncwarp();  // every lane is done with buffer nxt (the chunk before this one)
+                    stage_codes(s, sl, nxt, base + 32);
+                    cp_async_wait1();  // everything but that copy has landed: this chunk
                     __syncwarp();
-                    stage_codes(s, sl, buf, base);
+                } else if (cin && base > 0) {
                     cp_async_wait0();
                     __syncwarp();
                 }
+                const uint8_t* cb = &sm.codes[j][cur][0][lane];  // neighbour k's sign byte for this lane: cb[32 k]
+                const uint32_t* fb = &sm.flags[j][cur][0];
+                cur = nxt;
                 if (!fmode) {
                     const bool interior = __any_sync(0xffffffffu, lane < cnt && fb[lane] != 0u);
                     if (!interior) {

@@ -659,15 +659,24 @@ def scale_down(x, init_scale: float):
 
 
 def gaussian_batch(mean, nodes: int, lift_dim: int, eta: float, batch: int, stream: RngStream,
-                   workers: int = 1, device: Optional[int] = None) -> DenseState:
+                   workers: int = 1, device: Optional[int] = None, exact: Optional[bool] = None) -> DenseState:
+    """init.cpp:69-87.  exact (default in the fp64 precision mode): the reference's own host
+    libm normals, bit-identical (lcb_gaussian_batch_exact); otherwise device Box-Muller
+    (within a few ulp of glibc)."""
     mean = np.ascontiguousarray(mean, dtype=np.float64)
     if len(mean) != nodes * lift_dim:
         raise ShapeError(f"gaussian_batch: mean has {len(mean)} entries, expected "
                          f"{nodes * lift_dim}")
     s = DenseState(nodes, lift_dim, batch)
-    _check(_abi.lib().lcb_gaussian_batch(default_device() if device is None else device,
-                                         _ptr(mean), nodes, lift_dim, float(eta), batch,
-                                         stream.key(), _ptr(s.values)))
+    if exact is None:
+        exact = default_precision() == _abi.LCB_FP64
+    if exact:
+        _check(_abi.lib().lcb_gaussian_batch_exact(_ptr(mean), nodes, lift_dim, float(eta), batch,
+                                                   stream.key(), _ptr(s.values)))
+    else:
+        _check(_abi.lib().lcb_gaussian_batch(default_device() if device is None else device,
+                                             _ptr(mean), nodes, lift_dim, float(eta), batch,
+                                             stream.key(), _ptr(s.values)))
     return s
 
 

@@ -118,6 +118,8 @@ struct StepArgs {
     uint8_t* sgn_out;           // codes of x_out, or nullptr (not recorded)
     int64_t sgn_ld;             // bytes per row: (ld / span) * 32
     int64_t flag_off;           // K1s: byte offset of the per-row slab flags after the sign codes
+    unsigned* tile_ctr;         // K1s: [2] dynamic tile counters (this launch: [launch_seq & 1])
+    int64_t launch_seq;         // K1s: launches since the counters were zeroed
 };
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };

@@ -708,6 +708,8 @@ struct Work {
     DBuf<double> mean, dtrace, hostbatch;
     DBuf<int8_t> sign;
     DBuf<uint8_t> sgn;           // K1 saturation codes, one set per X buffer
+    DBuf<unsigned> tile_ctr;     // K1s dynamic tile counters [2]
+    int64_t stream_seq = 0;      // K1s launches on this workspace (counter parity)
     DBuf<float> dXm, dVm;        // dense path: member-major iterate / velocity of one column chunk
     DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes + K-step flags
     DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
@@ -1077,6 +1079,14 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         codes[0] = w.sgn.ensure(2 * bytes);
         codes[1] = codes[0] + bytes;
     }
+    if (use_stream) {
+        if (!w.tile_ctr.p) {
+            w.tile_ctr.ensure(2);
+            CK(cudaMemsetAsync(w.tile_ctr.p, 0, 2 * sizeof(unsigned), w.st));
+            w.stream_seq = 0;
+        }
+        a.tile_ctr = w.tile_ctr.p;
+    }
     if (use_stream && slab_outer) {
         // ---- K1s, slab-outer: for each 512-byte column slab, all its iterations
         CK(cudaEventRecord(w.ev0, w.st));
@@ -1106,6 +1116,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                     a.flags_cur = F + (t % 3) * members;
                     a.flags_zero = F + ((t + 1) % 3) * members;
                 }
+                a.launch_seq = w.stream_seq++;
                 launch_stream<T>(a, sl, 1, ee, w.st);
                 ++launches;
                 if (ee && ((t + 1) % 32 == 0) && t + 1 < ts) {  // stop once the slab's members left
@@ -1175,7 +1186,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             a.flags_zero = F + ((it + 1) % 3) * members;
         }
         if (use_stream)
+        {
+            a.launch_seq = w.stream_seq++;
             launch_stream<T>(a, 0, (a.W + sspan - 1) / sspan, ee, w.st);
+        }
         else
             launch_step<T>(a, ee, MODE_STEP, w.st);
         if (trace_host) {

@@ -238,55 +238,59 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         if (blockIdx.x == 0)
             for (int i = threadIdx.x; i < a.members; i += blockDim.x) a.flags_zero[i] = 0;
     }
+    // the tile counter of the NEXT launch (this launch uses tile_ctr[seq & 1], zeroed by the
+    // previous one; stream order keeps them apart)
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.tile_ctr[(a.launch_seq + 1) & 1] = 0u;
     __syncthreads();
 
     if (warp == 0) {
-        // ---------------- producer: this CTA's tiles t = blockIdx.x + i * gridDim.x, walked
-        // incrementally as (row tile, slab)
+        // ---------------- producer.  Tiles are claimed dynamically from a launch-wide counter
+        // (BA hubs make tiles uneven: a static split left config 5 at 62 % SM activity), P
+        // claims ahead, so the row_ptr loads of a claimed tile leave the critical path.  After
+        // the last tile a sentinel stage (slab = -1) tells the consumers to stop.
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
         }
         const uint64_t pol = policy_evict_first();
         constexpr int P = kLook;
-        int qrp[P];  // lane j <= R: row_ptr[min(r0 + j, n)] of the tile P ahead
-        const int drt = static_cast<int>(gridDim.x) % rowtiles, dsl = static_cast<int>(gridDim.x) / rowtiles;
-        int cur_rt = static_cast<int>(blockIdx.x) % rowtiles, cur_sl = static_cast<int>(blockIdx.x) / rowtiles;
-        int ah_rt = cur_rt, ah_sl = cur_sl;
-        auto adv = [&](int& rt, int& sl) {
-            rt += drt;
-            sl += dsl;
-            if (rt >= rowtiles) {
-                rt -= rowtiles;
-                ++sl;
-            }
-        };
-        auto fetch = [&]() {
+        int qrp[P], qt[P];  // per claim: lane j <= R: row_ptr[min(r0 + j, n)]; the tile index
+        unsigned* ctr = a.tile_ctr + (a.launch_seq & 1);
+        auto claim = [&](int& t) {
             int v = 0;
-            if (ah_sl < nslabs && lane <= kR) v = __ldg(a.row_ptr + min(ah_rt * kR + lane, a.n));
-            adv(ah_rt, ah_sl);
-            return v;
+            if (lane == 0) v = static_cast<int>(atomicAdd(ctr, 1u));
+            t = __shfl_sync(0xffffffffu, v, 0);
+            int rp = 0;
+            if (t < ntiles && lane <= kR) {
+                const int sl = t / rowtiles;
+                rp = __ldg(a.row_ptr + min((t - sl * rowtiles) * kR + lane, a.n));
+            }
+            return rp;
         };
 #pragma unroll
-        for (int q = 0; q < P; ++q) qrp[q] = fetch();
+        for (int q = 0; q < P; ++q) qrp[q] = claim(qt[q]);
         for (int i0 = 0;; i0 += P) {
             bool done = false;
 #pragma unroll
             for (int q = 0; q < P; ++q) {
                 const int i = i0 + q;
-                if (cur_sl >= nslabs) {
+                const int s = i % kStages;
+                if (i >= kStages) mbar_wait(&sm.empty[s], ((i / kStages) & 1) ^ 1);
+                const int t = qt[q];
+                if (t >= ntiles) {  // sentinel stage: no copies, a plain arrival
+                    if (lane == 0) {
+                        sm.slab[s] = -1;
+                        mbar_arrive(&sm.full[s]);
+                    }
                     done = true;
                     break;
                 }
                 const int beg = qrp[q];
-                qrp[q] = fetch();
+                qrp[q] = claim(qt[q]);
                 const int end = __shfl_down_sync(0xffffffffu, beg, 1);
                 const int first = __shfl_sync(0xffffffffu, beg, 0), last = __shfl_sync(0xffffffffu, beg, kR);
-                const int s = i % kStages;
-                if (i >= kStages) mbar_wait(&sm.empty[s], ((i / kStages) & 1) ^ 1);
-                int sl = cur_sl;
-                const int r0 = cur_rt * kR;
-                adv(cur_rt, cur_sl);
+                int sl = t / rowtiles;
+                const int r0 = (t - sl * rowtiles) * kR;
                 if (a.it & 1) sl = nslabs - 1 - sl;  // snake: reuse the slab just written
                 const int abeg = first & ~3;
                 const int ncopy = min(((last + 3) & ~3) - abeg, kColBuf);  // staged prefix of the tile's run
@@ -379,23 +383,22 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         cp_async_commit();
     };
 
-    const int my_tiles = (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
-                         static_cast<int>(gridDim.x);
-    if (my_tiles > 0) {
-        mbar_wait(&sm.full[0], 0);
-        stage_codes(0, sm.slab[0], 0, 0);
-    }
-    for (int i = 0; i < my_tiles; ++i) {
+    mbar_wait(&sm.full[0], 0);
+    bool have = sm.slab[0] >= 0;  // slab -1: the producer's end-of-work sentinel
+    if (have) stage_codes(0, sm.slab[0], 0, 0);
+    for (int i = 0; have; ++i) {
         const int s = i % kStages;
         const int sl = sm.slab[s];
         const int slab = slab0 + sl;
         if (slab != cur_slab) enter_slab(slab);
-        if (i + 1 < my_tiles) {  // the next tile's stage has normally landed (the producer runs ahead)
+        {  // the next tile's stage has normally landed (the producer runs ahead)
             const int sn = (i + 1) % kStages;
             mbar_wait(&sm.full[sn], ((i + 1) / kStages) & 1);
-            stage_codes(sn, sm.slab[sn], (i + 1) & 1, 0);
-        } else {
-            cp_async_commit();
+            have = sm.slab[sn] >= 0;
+            if (have)
+                stage_codes(sn, sm.slab[sn], (i + 1) & 1, 0);
+            else
+                cp_async_commit();
         }
         cp_async_wait1();  // this tile's code lines have landed
         __syncwarp();

@@ -138,10 +138,45 @@ __device__ __forceinline__ void planes_flush(uint32_t (&p)[16], uint32_t (&cnt)[
     for (int k = 0; k < 16; ++k) p[k] = 0;
 }
 
+// first-max argmax over `members` cuts in segments of seg_size, by one block
+__device__ void block_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
+                             unsigned long long* seg_keys) {
+    __shared__ unsigned long long red[32];
+    const int segs = (members + seg_size - 1) / seg_size;
+    for (int s = 0; s < segs; ++s) {
+        const int lo = s * seg_size, hi = min(members, lo + seg_size);
+        unsigned long long best = 0;
+        for (int m = lo + threadIdx.x; m < hi; m += blockDim.x) {
+            const unsigned long long gm = static_cast<unsigned long long>(member_base + (m - lo));
+            const unsigned long long key = (__ldcg(cuts + m) << 32) | (0xffffffffull - gm);
+            best = key > best ? key : best;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+            best = t > best ? t : best;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                best = t > best ? t : best;
+            }
+            if (threadIdx.x == 0) seg_keys[s] = best;
+        }
+        __syncthreads();
+    }
+}
+
+// Fused epilogue: bit-sliced cut counts, then -- in the last block to finish -- the
+// first-max argmax of every segment (one launch instead of two; seg_keys null: counts only).
 __global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_ptr,
                                                    const int* __restrict__ col,
                                                    const uint32_t* __restrict__ Z, int n,
-                                                   unsigned long long* __restrict__ cuts) {
+                                                   unsigned long long* __restrict__ cuts,
+                                                   unsigned long long* __restrict__ done, int members, int seg_size,
+                                                   int64_t member_base, unsigned long long* __restrict__ seg_keys) {
     const int w = blockIdx.y;
     const uint32_t* zw = Z + static_cast<int64_t>(w) * n;
     uint32_t planes[16];
@@ -174,6 +209,16 @@ __global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_p
         if (lane == b) mine = t;
     }
     if (mine) atomicAdd(cuts + w * 32 + lane, static_cast<unsigned long long>(mine));
+    if (seg_keys == nullptr) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        last = atomicAdd(done, 1ull) == static_cast<unsigned long long>(gridDim.x) * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    block_argmax(cuts, members, seg_size, member_base, seg_keys);
 }
 
 // ---------------------------------------------------------------------------
@@ -304,7 +349,17 @@ void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned 
     cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * static_cast<size_t>(words) * 32, s);
     const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
     count_launch();
-    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts);
+    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, nullptr, 0, 1, 0, nullptr);
+}
+
+void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts, int members,
+                       int seg_size, int64_t member_base, unsigned long long* seg_keys, cudaStream_t s) {
+    // cuts [words * 32] followed by the block-completion counter, zeroed together
+    cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * (static_cast<size_t>(words) * 32 + 1), s);
+    const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
+    count_launch();
+    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, cuts + words * 32, members,
+                                                       seg_size, member_base, seg_keys);
 }
 
 void launch_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,

@@ -206,6 +206,9 @@ void launch_max_u32(const uint32_t* a, int64_t count, unsigned* out, cudaStream_
 // bit-sliced cut counts per member (cuts zeroed inside)
 void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts,
                       cudaStream_t s);
+// fused: cut counts + (last block) first-max argmax per segment; cuts needs words*32 + 1 entries
+void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts, int members,
+                       int seg_size, int64_t member_base, unsigned long long* seg_keys, cudaStream_t s);
 // segment argmax of packed keys; seg_keys[s] = max over members of segment s
 void launch_argmax(const unsigned long long* cuts, int members, int seg_size,
                    int64_t member_base, unsigned long long* seg_keys, cudaStream_t s);

@@ -1451,10 +1451,9 @@ struct Solver {
         const int words = static_cast<int>((B + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * n);
         launch_round_pack<T>(w.X[ir.final_buf].p, w.ld, n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
-        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32);
-        launch_cut_count(g, Z, words, cuts, w.st);
+        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32 + 1);
         unsigned long long* key = w.keys.ensure(8);
-        launch_argmax(cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
+        launch_cut_argmax(g, Z, words, cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
         comm_allreduce(comm, key, 1, 8, true, w.st, "allreduce(key)");
         launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
         comm_allreduce(comm, w.win.p, static_cast<size_t>(words_n), 4, true, w.st, "allreduce(winner)");
@@ -1527,10 +1526,9 @@ struct Solver {
         const int words = (members + 31) / 32;
         out.Z = w.Z.ensure(static_cast<size_t>(words) * n);
         launch_round_pack<T>(w.X[ir.final_buf].p, w.ld, n, members, l, lifted ? 1 : 0, out.Z, w.st);
-        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32);
-        launch_cut_count(g, out.Z, words, cuts, w.st);
+        unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32 + 1);
         out.d_keys = w.keys.ensure(static_cast<size_t>(std::max(K, 8)));
-        launch_argmax(cuts, members, static_cast<int>(B), member_base, out.d_keys, w.st);
+        launch_cut_argmax(g, out.Z, words, cuts, members, static_cast<int>(B), member_base, out.d_keys, w.st);
         comm_allreduce(comm, out.d_keys, static_cast<size_t>(K), 8, true, w.st, "allreduce(keys)");
         d2h(w.h_keys, out.d_keys, sizeof(unsigned long long) * K, w.st);
         CK(cudaStreamSynchronize(w.st));
@@ -2301,10 +2299,9 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
         const int words = static_cast<int>((B + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
         launch_round_pack<double>(w.X[0].p, w.ld, G.n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
-        unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32);
-        launch_cut_count(G, Z, words, c, w.st);
+        unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32 + 1);
         unsigned long long* key = w.keys.ensure(8);
-        launch_argmax(c, static_cast<int>(B), static_cast<int>(B), 0, key, w.st);
+        launch_cut_argmax(G, Z, words, c, static_cast<int>(B), static_cast<int>(B), 0, key, w.st);
         uint32_t* bits = w.win.ensure((G.n + 31) / 32);
         launch_extract_winner(Z, G.n, key, 0, static_cast<int>(B), bits, w.st);
         std::vector<unsigned long long> hc(static_cast<size_t>(B));

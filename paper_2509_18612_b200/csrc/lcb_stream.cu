@@ -233,13 +233,19 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             mbar_init(&sm.empty[s], kR);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
     }
+    // Programmatic dependent launch: everything above overlaps the previous iteration's tail;
+    // nothing the previous launch writes (iterate, codes, flags, counters) is touched before
+    // this wait for its completion.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (EE) {
         if (blockIdx.x == 0)
             for (int i = threadIdx.x; i < a.members; i += blockDim.x) a.flags_zero[i] = 0;
     }
     // the tile counter of the NEXT launch (this launch uses tile_ctr[seq & 1], zeroed by the
-    // previous one; stream order keeps them apart)
+    // previous one)
     if (blockIdx.x == 0 && threadIdx.x == 0) a.tile_ctr[(a.launch_seq + 1) & 1] = 0u;
     __syncthreads();
 
@@ -248,10 +254,6 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         // (BA hubs make tiles uneven: a static split left config 5 at 62 % SM activity), P
         // claims ahead, so the row_ptr loads of a claimed tile leave the critical path.  After
         // the last tile a sentinel stage (slab = -1) tells the consumers to stop.
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mx)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mv)) : "memory");
-        }
         const uint64_t pol = policy_evict_first();
         constexpr int P = kLook;
         int qrp[P], qt[P];  // per claim: lane j <= R: row_ptr[min(r0 + j, n)]; the tile index
@@ -281,6 +283,8 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                     if (lane == 0) {
                         sm.slab[s] = -1;
                         mbar_arrive(&sm.full[s]);
+                        // this CTA claims no more tiles: the next launch may start its prologue
+                        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
                     }
                     done = true;
                     break;
@@ -659,7 +663,18 @@ void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
     slab_map(&mx, a.x_in, a.ld, a.n, static_cast<int>(sizeof(T)));
     slab_map(&mv, a.vel, a.ld, a.n, static_cast<int>(sizeof(T)));
     count_launch();
-    k_stream<T, GEN, EE><<<grid, kThreadsS, smem, st>>>(a, rowtiles, slab0, nslabs, mx, mv);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreadsS);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, k_stream<T, GEN, EE>, a, rowtiles, slab0, nslabs, mx, mv),
+               "cudaLaunchKernelEx(k_stream)");
 }
 
 }  // namespace

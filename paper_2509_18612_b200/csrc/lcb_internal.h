@@ -120,6 +120,7 @@ struct StepArgs {
     int64_t flag_off;           // K1s: byte offset of the per-row slab flags after the sign codes
     unsigned* tile_ctr;         // K1s: [2] dynamic tile counters (this launch: [launch_seq & 1])
     int64_t launch_seq;         // K1s: launches since the counters were zeroed
+    int xskip;                  // K1s: a row slab whose flag is 0 keeps x only in its sign code
 };
 
 enum StepMode { MODE_STEP = 0, MODE_LAPLACE = 1 };
@@ -186,6 +187,11 @@ int step_span(int W);  // columns covered by one warp for this W
 template <typename T>
 void launch_stream(const StepArgs<T>& a, int slab0, int nslabs, bool early_exit, cudaStream_t s);
 int stream_slab_cols(int elem_bytes);  // columns of one K1s slab (1 KB of a row)
+// write +-1 from the sign codes into X for every row slab whose flag is 0 (x-code mode:
+// those slabs were not stored by K1s); codes/flags [nslabs][n], slab sl at column slab0 + sl
+template <typename T>
+void launch_xcode_fill(T* X, int64_t ld, int n, const uint8_t* codes, int64_t flag_off, int slab0, int nslabs,
+                       cudaStream_t s);
 
 template <typename T>
 void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s);
@@ -261,6 +267,7 @@ enum Opt : int {
     OPT_BANK_REFINE,   // refinement passes of that order
     OPT_DENSE,         // K3 adjacency at graph creation: -1 auto, 0 never, 1 always
     OPT_SLAB_OUTER,    // K1s order: -1 auto (codes beyond L2), 0 iteration-major, 1 slab-major
+    OPT_XCODE,         // K1s: saturated row slabs keep x in the sign code only (1 on, 0 off)
     OPT_COUNT
 };
 int64_t option(Opt o);

@@ -78,6 +78,7 @@ constexpr OptDef kOptDefs[OPT_COUNT] = {
     {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", 1},         {"signrec", "LCB_SIGNREC", -1},
     {"chunk", "LCB_CHUNK", 0},        {"res_split", "LCB_RES_SPLIT", 1},   {"bank_order", "LCB_BANK_ORDER", 2},
     {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1}, {"slab_outer", "LCB_SLAB_OUTER", -1},
+    {"xcode", "LCB_XCODE", 1},
 };
 std::atomic<int64_t> g_opts[OPT_COUNT];
 std::once_flag g_opts_once;
@@ -1086,6 +1087,11 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
             w.stream_seq = 0;
         }
         a.tile_ctr = w.tile_ctr.p;
+        // x-code mode (OPT_XCODE): row slabs on the box corners are stored as their sign codes
+        // only, X is completed by launch_xcode_fill after a slab's (or the run's) last
+        // iteration.  Not with per-segment stop iterations: a stopped segment's X must stay
+        // complete while later iterations overwrite the codes.
+        a.xskip = (option(OPT_XCODE) != 0 && !seg_iters) ? 1 : 0;
     }
     if (use_stream && slab_outer) {
         // ---- K1s, slab-outer: for each 512-byte column slab, all its iterations
@@ -1130,6 +1136,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                         break;
                     }
                 }
+            }
+            if (a.xskip && t > 0) {
+                launch_xcode_fill<T>(w.X[t & 1].p, w.ld, g.n, codes[t & 1], a.flag_off, sl, 1, w.st);
+                ++w.step_launches;
             }
             slab_it[static_cast<size_t>(sl)] = t;
             it_max = std::max(it_max, t);
@@ -1217,6 +1227,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                 break;
             }
         }
+    }
+    if (use_stream && a.xskip && it > 0) {
+        launch_xcode_fill<T>(w.X[it & 1].p, w.ld, g.n, codes[it & 1], a.flag_off, 0, nslabs, w.st);
+        ++w.step_launches;
     }
     if (seg_iters) {
         // a segment that stopped at T_s left its final iterate in X[T_s & 1]

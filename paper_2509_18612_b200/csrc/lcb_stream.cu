@@ -64,6 +64,14 @@ constexpr int kSlab = 1024;             // bytes of one row of a slab
 #define LCB_STREAM_FNB 2
 #endif
 constexpr int kFNB = LCB_STREAM_FNB;    // interior-neighbour gathers in flight (fp mode)
+#ifndef LCB_STREAM_D
+#define LCB_STREAM_D 1
+#endif
+// tiles whose neighbour code lines are in flight ahead of the one being summed: the code
+// gathers are L2 round trips, so one tile of lookahead left the steady state latency-bound
+constexpr int kD = LCB_STREAM_D;
+constexpr int kCB = kD + 2;             // code buffers per warp: kD + 1 tiles + the hub chunk
+static_assert(kD < kStages, "code lookahead needs the tiles' stages");
 
 template <typename T>
 struct Lanes {
@@ -128,6 +136,10 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // 16-byte vectors of a lane's half-slab
 __device__ __forceinline__ void ld16(float* v, const void* smem) {
@@ -147,6 +159,19 @@ __device__ __forceinline__ void ldg16(float* v, const float* p) {
 }
 __device__ __forceinline__ void ldg16(double* v, const double* p) {
     const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = q.x;
+    v[1] = q.y;
+}
+// streaming (evict-first) 16-byte loads of data read once
+__device__ __forceinline__ void ldcs16(float* v, const float* p) {
+    const float4 q = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+}
+__device__ __forceinline__ void ldcs16(double* v, const double* p) {
+    const double2 q = __ldcs(reinterpret_cast<const double2*>(p));
     v[0] = q.x;
     v[1] = q.y;
 }
@@ -206,11 +231,14 @@ struct StreamSmem {
     int beg[kStages][kR];
     int deg[kStages][kR];
     int coff[kStages][kR];
+    int xfl[kStages][kR];            // x-code mode: 0 = the row slab's x is its sign code
+    int xbox[kStages];               // 1: the stage holds the tile's x box
     int slab[kStages];               // launch-relative slab of the tile in the stage
-    // per consumer warp: code lines of <= 32 neighbours (this row, the next tile's row, and a
-    // third buffer that double-buffers the further 32-neighbour chunks of hub rows)
-    alignas(16) uint8_t codes[kR][3][32][32];
-    uint32_t flags[kR][3][32];       // and their "slab not saturated" flags
+    // per consumer warp: code lines of <= 32 neighbours (this row, the rows of the next kD
+    // tiles, and one more buffer that double-buffers the further 32-neighbour chunks of hub rows)
+    alignas(16) uint8_t codes[kR][kCB][32][32];
+    uint32_t flags[kR][kCB][32];     // and their "slab not saturated" flags
+    alignas(16) uint8_t own[kR][kD + 1][32];  // x-code mode: the row's own code line
     uint64_t full[kStages];
     uint64_t empty[kStages];
 };
@@ -256,21 +284,31 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         // the last tile a sentinel stage (slab = -1) tells the consumers to stop.
         const uint64_t pol = policy_evict_first();
         constexpr int P = kLook;
-        int qrp[P], qt[P];  // per claim: lane j <= R: row_ptr[min(r0 + j, n)]; the tile index
+        // per claim: lane j <= R: row_ptr[min(r0 + j, n)]; the tile index; lane j < R: the
+        // flag of row r0 + j's slab in the input codes (x-code mode; 0 = x is in the code)
+        int qrp[P], qt[P], qfl[P];
         unsigned* ctr = a.tile_ctr + (a.launch_seq & 1);
-        auto claim = [&](int& t) {
+        const uint32_t* const pfin =
+            (a.xskip && a.sgn_in) ? reinterpret_cast<const uint32_t*>(a.sgn_in + a.flag_off) : nullptr;
+        auto claim = [&](int& t, int& fl) {
             int v = 0;
             if (lane == 0) v = static_cast<int>(atomicAdd(ctr, 1u));
             t = __shfl_sync(0xffffffffu, v, 0);
             int rp = 0;
+            fl = 1;
             if (t < ntiles && lane <= kR) {
-                const int sl = t / rowtiles;
-                rp = __ldg(a.row_ptr + min((t - sl * rowtiles) * kR + lane, a.n));
+                int sl = t / rowtiles;
+                const int row = (t - sl * rowtiles) * kR + lane;
+                rp = __ldg(a.row_ptr + min(row, a.n));
+                if (pfin && lane < kR) {
+                    if (a.it & 1) sl = nslabs - 1 - sl;
+                    fl = row < a.n ? static_cast<int>(__ldcg(pfin + static_cast<uint32_t>(sl) * n32 + row)) : 0;
+                }
             }
             return rp;
         };
 #pragma unroll
-        for (int q = 0; q < P; ++q) qrp[q] = claim(qt[q]);
+        for (int q = 0; q < P; ++q) qrp[q] = claim(qt[q], qfl[q]);
         for (int i0 = 0;; i0 += P) {
             bool done = false;
 #pragma unroll
@@ -290,7 +328,8 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                     break;
                 }
                 const int beg = qrp[q];
-                qrp[q] = claim(qt[q]);
+                const int fl = qfl[q];
+                qrp[q] = claim(qt[q], qfl[q]);
                 const int end = __shfl_down_sync(0xffffffffu, beg, 1);
                 const int first = __shfl_sync(0xffffffffu, beg, 0), last = __shfl_sync(0xffffffffu, beg, kR);
                 int sl = t / rowtiles;
@@ -306,11 +345,16 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                     sm.beg[s][lane] = beg;
                     sm.deg[s][lane] = ok ? end - beg : 0;
                     sm.coff[s][lane] = (ok && end - abeg <= ncopy) ? beg - abeg : -1;
+                    sm.xfl[s][lane] = fl;
                 }
+                // the x box only when every row slab of the tile needs its stored x; otherwise the
+                // rows whose x is not in the codes load it themselves (consumer ldg)
+                const bool skipx = !__all_sync(0xffffffffu, lane >= kR || fl != 0);
+                if (lane == 0) sm.xbox[s] = skipx ? 0 : 1;
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_expect_tx(&sm.full[s], 2u * kR * kSlab + static_cast<uint32_t>(ncopy) * 4u);
-                    tma_tile(&sm.x[s][0][0], &mx, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
+                    mbar_expect_tx(&sm.full[s], (skipx ? 1u : 2u) * kR * kSlab + static_cast<uint32_t>(ncopy) * 4u);
+                    if (!skipx) tma_tile(&sm.x[s][0][0], &mx, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
                     tma_tile(&sm.v[s][0][0], &mv, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
                     if (ncopy > 0)
                         bulk_g2s(&sm.col[s][0], a.col + abeg, static_cast<uint32_t>(ncopy) * 4u, &sm.full[s], pol);
@@ -383,34 +427,66 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 cp_async16(&sm.codes[j][buf][lane][16], cin + line * 32u + 16u);
                 cp_async4(&sm.flags[j][buf][lane], fin + line);
             }
+            if (k0 == 0 && lane >= 24 && a.xskip && sm.xfl[st][j] == 0) {  // own line, 4 bytes per lane
+                const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(row);
+                cp_async4(&sm.own[j][buf][4 * (lane - 24)], cin + line * 32u + 4u * (lane - 24));
+            }
         }
         cp_async_commit();
     };
 
+    // tiles i .. i + kD have their code lines in flight (one cp.async group per tile; an empty
+    // group past the end); have[d]: tile i + d exists (slab -1: the producer's sentinel)
+    bool have[kD + 1];
+#pragma unroll
+    for (int d = 0; d <= kD; ++d) have[d] = false;
     mbar_wait(&sm.full[0], 0);
-    bool have = sm.slab[0] >= 0;  // slab -1: the producer's end-of-work sentinel
-    if (have) stage_codes(0, sm.slab[0], 0, 0);
-    for (int i = 0; have; ++i) {
+    have[0] = sm.slab[0] >= 0;
+    if (have[0]) stage_codes(0, sm.slab[0], 0, 0);
+#pragma unroll
+    for (int d = 1; d < kD; ++d) {
+        if (have[d - 1]) {
+            mbar_wait(&sm.full[d % kStages], (d / kStages) & 1);
+            have[d] = sm.slab[d % kStages] >= 0;
+        }
+        if (have[d])
+            stage_codes(d % kStages, sm.slab[d % kStages], d, 0);
+        else
+            cp_async_commit();
+    }
+    for (int i = 0; have[0]; ++i) {
         const int s = i % kStages;
         const int sl = sm.slab[s];
         const int slab = slab0 + sl;
         if (slab != cur_slab) enter_slab(slab);
-        {  // the next tile's stage has normally landed (the producer runs ahead)
-            const int sn = (i + 1) % kStages;
-            mbar_wait(&sm.full[sn], ((i + 1) / kStages) & 1);
-            have = sm.slab[sn] >= 0;
-            if (have)
-                stage_codes(sn, sm.slab[sn], (i + 1) & 1, 0);
-            else
-                cp_async_commit();
+        have[kD] = false;
+        if (have[kD - 1]) {  // tile i + kD's stage has normally landed (the producer runs ahead)
+            const int sn = (i + kD) % kStages;
+            mbar_wait(&sm.full[sn], ((i + kD) / kStages) & 1);
+            have[kD] = sm.slab[sn] >= 0;
         }
-        cp_async_wait1();  // this tile's code lines have landed
+        if (have[kD])
+            stage_codes((i + kD) % kStages, sm.slab[(i + kD) % kStages], (i + kD) % (kD + 1), 0);
+        else
+            cp_async_commit();
+        cp_async_wait_n<kD>();  // this tile's code lines have landed
         __syncwarp();
         const int row = sm.row[s][j];
         if (row >= 0) {
             const int deg = sm.deg[s][j];
             const int coff = sm.coff[s][j];
-            const int buf = i & 1;
+            // x-code mode: this row slab was not stored last iteration, its x is the sign code
+            const bool own_code = a.xskip && cin && sm.xfl[s][j] == 0;
+            const int buf = i % (kD + 1);
+            const uint32_t own_bits = own_code ? sm.own[j][buf][lane] : 0u;
+            // stored x outside a loaded box: issued now, consumed by the epilogue
+            const bool own_ld = !own_code && sm.xbox[s] == 0;
+            T xg[E];
+            if (own_ld) {
+                const T* p = a.x_in + static_cast<int64_t>(row) * a.ld + col_of(slab, 0);
+                ldcs16(&xg[0], p);
+                ldcs16(&xg[H], p + SPAN / 2);
+            }
             int cur = buf;  // buffer holding the current 32-neighbour chunk
             const T* xin0 = a.x_in + col_of(slab, 0);
             const T* xin1 = xin0 + SPAN / 2;
@@ -430,10 +506,12 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 const int cnt = min(32, deg - base);
                 int nxt = cur;
                 if (cin && base + 32 < deg) {  // hub rows: stage the next chunk while this one is summed
-                    nxt = cur == 2 ? buf : 2;
+                    nxt = cur == kD + 1 ? buf : kD + 1;
                     __syncwarp();  // every lane is done with buffer nxt (the chunk before this one)
                     stage_codes(s, sl, nxt, base + 32);
-                    cp_async_wait1();  // everything but that copy has landed: this chunk
+                    // chunk 0 landed with the tile's group; later chunks: everything but the copy
+                    // just issued (the lookahead tiles' groups are older and complete with it)
+                    if (base > 0) cp_async_wait1();
                     __syncwarp();
                 } else if (cin && base > 0) {
                     cp_async_wait0();
@@ -525,8 +603,16 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 
             // ---- epilogue (ascent.cpp:66-77)
             T xv[E], vv[E];
-            ld16(&xv[0], &sm.x[s][j][16 * lane]);
-            ld16(&xv[H], &sm.x[s][j][512 + 16 * lane]);
+            if (own_code) {  // x on the box corners, exactly: +-1 from the sign bits
+#pragma unroll
+                for (int e = 0; e < E; ++e) xv[e] = ((own_bits >> e) & 1u) ? T(1) : T(-1);
+            } else if (own_ld) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) xv[e] = xg[e];
+            } else {
+                ld16(&xv[0], &sm.x[s][j][16 * lane]);
+                ld16(&xv[H], &sm.x[s][j][512 + 16 * lane]);
+            }
             ld16(&vv[0], &sm.v[s][j][16 * lane]);
             ld16(&vv[H], &sm.v[s][j][512 + 16 * lane]);
             const T dg = static_cast<T>(deg);
@@ -590,19 +676,25 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             }
             T* xo0 = a.x_out + static_cast<int64_t>(row) * a.ld + col_of(slab, 0);
             T* vo0 = a.vel + static_cast<int64_t>(row) * a.ld + col_of(slab, 0);
-            stg16(xo0, &xo[0]);
-            stg16(xo0 + SPAN / 2, &xo[H]);
+            const bool any_interior = __any_sync(0xffffffffu, interior);
+            // x-code mode: a row slab entirely on the box corners is stored as its sign code only
+            // (readers take +-1 from it; launch_xcode_fill writes X after the last iteration)
+            if (!(a.xskip && cout) || any_interior) {
+                stg16(xo0, &xo[0]);
+                stg16(xo0 + SPAN / 2, &xo[H]);
+            }
             stg16(vo0, &vv[0]);
             stg16(vo0 + SPAN / 2, &vv[H]);
             if (cout) {
                 const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(row);
                 cout[line * 32u + lane] = static_cast<uint8_t>(sign);
-                const bool any_interior = __any_sync(0xffffffffu, interior);
                 if (lane == 0) fout[line] = any_interior ? 1u : 0u;
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
+#pragma unroll
+        for (int d = 0; d < kD; ++d) have[d] = have[d + 1];
     }
     if (cur_slab >= 0) flush_bits();
 }
@@ -677,7 +769,43 @@ void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
                "cudaLaunchKernelEx(k_stream)");
 }
 
+// one warp per (slab, row): +-1 from the sign byte of each lane for row slabs with flag 0
+template <typename T>
+__global__ void k_xcode_fill(T* X, int64_t ld, int n, const uint8_t* codes, int64_t flag_off, int slab0,
+                             int nslabs) {
+    constexpr int E = Lanes<T>::E, H = Lanes<T>::H, SPAN = Lanes<T>::SPAN;
+    const uint32_t* flags = reinterpret_cast<const uint32_t*>(codes + flag_off);
+    const int lane = threadIdx.x & 31;
+    const int64_t lines = static_cast<int64_t>(n) * nslabs;
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < lines;
+         w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        if (flags[w] != 0u) continue;
+        const int sl = static_cast<int>(w / n);
+        const int row = static_cast<int>(w - static_cast<int64_t>(sl) * n);
+        const uint32_t b = codes[w * 32 + lane];
+        T xo[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) xo[e] = ((b >> e) & 1u) ? T(1) : T(-1);
+        T* p = X + static_cast<int64_t>(row) * ld + static_cast<int64_t>(slab0 + sl) * SPAN + lane * H;
+        stg16(p, &xo[0]);
+        stg16(p + SPAN / 2, &xo[H]);
+    }
+}
+
 }  // namespace
+
+template <typename T>
+void launch_xcode_fill(T* X, int64_t ld, int n, const uint8_t* codes, int64_t flag_off, int slab0, int nslabs,
+                       cudaStream_t s) {
+    const int64_t lines = static_cast<int64_t>(n) * nslabs;
+    if (lines <= 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((lines + 7) / 8, 16 * num_sms(-1)));
+    count_launch();
+    k_xcode_fill<T><<<grid, 256, 0, s>>>(X, ld, n, codes, flag_off, slab0, nslabs);
+    cuda_check(cudaGetLastError(), "k_xcode_fill");
+}
+template void launch_xcode_fill<float>(float*, int64_t, int, const uint8_t*, int64_t, int, int, cudaStream_t);
+template void launch_xcode_fill<double>(double*, int64_t, int, const uint8_t*, int64_t, int, int, cudaStream_t);
 
 int stream_slab_cols(int elem_bytes) { return kSlab / elem_bytes; }
 

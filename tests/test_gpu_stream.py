@@ -9,6 +9,9 @@ take).  Forced here with the library knobs resident=0 (no K2) and stream=1.
   graphs), >= 99 % identical cuts at full T.
 * the batched-search path (per-member alpha / T, shrinking live width) bit-exact.
 * one iterate larger than L2 (126 MB) in fp64, bit-exact.
+* x-code mode (row slabs on the box corners stored as sign codes only, X completed after
+  the last iteration) on and off: fp64 bit-exact with the oracle either way, fp32 on ==
+  off bit for bit.
 """
 import numpy as np
 import pytest
@@ -26,10 +29,10 @@ def pg(c):
     return lc.Graph.from_csr(c.n, c.off, c.adj)
 
 
-def run(g, x, n, l, B, alpha, T, mu, ee, prec, slab_outer=-1):
+def run(g, x, n, l, B, alpha, T, mu, ee, prec, slab_outer=-1, xcode=1):
     s = lc.DenseState(n, l, B)
     s.values[:] = x
-    with lc.options(resident=0, stream=1, chunk=0, slab_outer=slab_outer):
+    with lc.options(resident=0, stream=1, chunk=0, slab_outer=slab_outer, xcode=xcode):
         lc.ascend(g, s, lc.AscentParams(alpha, T, mu, ee), precision=prec)
     return s.values
 
@@ -53,17 +56,38 @@ def start(rng, n, l, B):
     return rng.choice([-1e-4, 1e-4], B * l * n) + rng.normal(0, 9e-5, B * l * n)
 
 
+@pytest.mark.parametrize("xcode", [1, 0])
 @pytest.mark.parametrize("slab_outer", [0, 1])
 @pytest.mark.parametrize("l,B,ee", [(1, 100, False), (1, 100, True), (2, 70, False), (2, 70, True),
-                                    (3, 45, False), (3, 45, True), (1, 300, False)])
-def test_stream_fp64_bitwise_through_saturation(l, B, ee, slab_outer):
+                                    (3, 45, False), (3, 45, True), (1, 300, False), (1, 256, True)])
+def test_stream_fp64_bitwise_through_saturation(l, B, ee, slab_outer, xcode):
     cg = ba_like(2600, 4, 3)          # hubs (degree > 100), BA skew
     rng = np.random.default_rng(l * 100 + B)
     x = start(rng, cg.n, l, B)
     for T in (1, 7, 60):              # 60: well past saturation -> code path
         want, _ = O.ascend(cg, x, l, B, 0.05, T, 0.9, ee)
-        got = run(pg(cg), x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP64, slab_outer)
+        got = run(pg(cg), x, cg.n, l, B, 0.05, T, 0.9, ee, LCB_FP64, slab_outer, xcode)
         assert np.array_equal(got, want), (l, B, ee, T)
+
+
+@pytest.mark.parametrize("slab_outer", [0, 1])
+def test_stream_xcode_fp32_on_equals_off(slab_outer):
+    """fp32, full slabs (no padding columns): most row slabs reach the corners and are
+    stored as codes only; the final X (after the fill) equals the fully stored run bit for
+    bit at every T, odd and even."""
+    rng = np.random.default_rng(21)
+    n = 30_000
+    u, v = rng.integers(0, n, 150_000), rng.integers(0, n, 150_000)
+    keep = u != v
+    cg = O.csr_from_edges(n, u[keep], v[keep])
+    g = pg(cg)
+    B = 512
+    x = start(rng, n, 1, B)
+    for T in (1, 2, 41, 120):
+        on = run(g, x, n, 1, B, 0.05, T, 0.9, False, LCB_FP32, slab_outer, 1)
+        off = run(g, x, n, 1, B, 0.05, T, 0.9, False, LCB_FP32, slab_outer, 0)
+        assert np.array_equal(on, off), T
+    assert np.mean(np.abs(on) == 1.0) > 0.9  # the code-only path was exercised
 
 
 def test_stream_fp64_low_skew_natural_order_and_isolated_rows():

@@ -375,8 +375,12 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     }
     g.deg_var = acc / nn;
     g.deg_sd = std::sqrt(g.deg_var);
-    std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return deg[a] > deg[b]; });
+    {  // rows by descending degree, ties in id order: a stable counting sort, O(n + max degree)
+        std::vector<int64_t> start(static_cast<size_t>(maxd) + 2, 0);
+        for (uint32_t v = 0; v < n; ++v) ++start[static_cast<size_t>(maxd - deg[v]) + 1];
+        for (size_t d = 1; d < start.size(); ++d) start[d] += start[d - 1];
+        for (uint32_t v = 0; v < n; ++v) ord[static_cast<size_t>(start[static_cast<size_t>(maxd - deg[v])]++)] = static_cast<int>(v);
+    }
 
     DeviceScope ds(device);
     CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));

@@ -223,9 +223,26 @@ __device__ __forceinline__ void pga_raw_neg2(const double* x, const double* nax,
     raw[1] = pga_raw(x[1], -nax[1], v[1], alpha, mu, dg);
 }
 
+#ifndef LCB_STREAM_CLAIM
+#define LCB_STREAM_CLAIM 1
+#endif
+constexpr int kClaim = LCB_STREAM_CLAIM;  // tiles per dynamic claim
+#ifndef LCB_STREAM_STATIC
+#define LCB_STREAM_STATIC 0
+#endif
+#ifndef LCB_STREAM_EXP
+#define LCB_STREAM_EXP 0  // timing experiments only (wrong results): 1 consumers idle, 2 no v box
+#endif
+#ifndef LCB_STREAM_XBOX
+#define LCB_STREAM_XBOX 1
+#endif
+// 1: the producer stages the tile's x box when every row needs its stored x; 0: consumers
+// always load their own stored x (the SMEM goes to deeper v staging)
+constexpr bool kXBox = LCB_STREAM_XBOX != 0;
+
 struct StreamSmem {
-    unsigned char x[kStages][kR][kSlab];
-    unsigned char v[kStages][kR][kSlab];
+    alignas(128) unsigned char x[kXBox ? kStages : 1][kXBox ? kR : 1][kXBox ? kSlab : 128];
+    alignas(128) unsigned char v[kStages][kR][kSlab];
     int col[kStages][kColBuf];
     int row[kStages][kR];
     int beg[kStages][kR];
@@ -290,9 +307,25 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         unsigned* ctr = a.tile_ctr + (a.launch_seq & 1);
         const uint32_t* const pfin =
             (a.xskip && a.sgn_in) ? reinterpret_cast<const uint32_t*>(a.sgn_in + a.flag_off) : nullptr;
+        // tiles are claimed kClaim at a time (one atomic per kClaim tiles: same-address
+        // atomics from every SM serialise in one L2 slice)
+        int cbase = 0, cleft = 0;  // lane 0's current claim: next tile, tiles left in it
+        int sidx = 0;              // static experiment: this CTA's next tile
         auto claim = [&](int& t, int& fl) {
             int v = 0;
-            if (lane == 0) v = static_cast<int>(atomicAdd(ctr, 1u));
+#if LCB_STREAM_STATIC
+            v = static_cast<int>(blockIdx.x) + sidx * static_cast<int>(gridDim.x);
+            ++sidx;
+#else
+            if (lane == 0) {
+                if (cleft == 0) {
+                    cbase = static_cast<int>(atomicAdd(ctr, static_cast<unsigned>(kClaim)));
+                    cleft = kClaim;
+                }
+                v = cbase++;
+                --cleft;
+            }
+#endif
             t = __shfl_sync(0xffffffffu, v, 0);
             int rp = 0;
             fl = 1;
@@ -349,13 +382,19 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 }
                 // the x box only when every row slab of the tile needs its stored x; otherwise the
                 // rows whose x is not in the codes load it themselves (consumer ldg)
-                const bool skipx = !__all_sync(0xffffffffu, lane >= kR || fl != 0);
+                const bool skipx = !kXBox || !__all_sync(0xffffffffu, lane >= kR || fl != 0);
                 if (lane == 0) sm.xbox[s] = skipx ? 0 : 1;
                 __syncwarp();
                 if (lane == 0) {
+#if LCB_STREAM_EXP == 2  // timing experiment: no v box
+                    mbar_expect_tx(&sm.full[s], (skipx ? 0u : 1u) * kR * kSlab + static_cast<uint32_t>(ncopy) * 4u);
+#else
                     mbar_expect_tx(&sm.full[s], (skipx ? 1u : 2u) * kR * kSlab + static_cast<uint32_t>(ncopy) * 4u);
-                    if (!skipx) tma_tile(&sm.x[s][0][0], &mx, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
+#endif
+                    if (kXBox && !skipx) tma_tile(&sm.x[kXBox ? s : 0][0][0], &mx, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
+#if LCB_STREAM_EXP != 2
                     tma_tile(&sm.v[s][0][0], &mv, (slab0 + sl) * SPAN, r0, &sm.full[s], pol);
+#endif
                     if (ncopy > 0)
                         bulk_g2s(&sm.col[s][0], a.col + abeg, static_cast<uint32_t>(ncopy) * 4u, &sm.full[s], pol);
                 }
@@ -472,7 +511,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         cp_async_wait_n<kD>();  // this tile's code lines have landed
         __syncwarp();
         const int row = sm.row[s][j];
-        if (row >= 0) {
+        if (row >= 0 && LCB_STREAM_EXP != 1) {
             const int deg = sm.deg[s][j];
             const int coff = sm.coff[s][j];
             // x-code mode: this row slab was not stored last iteration, its x is the sign code
@@ -487,118 +526,150 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 ldcs16(&xg[0], p);
                 ldcs16(&xg[H], p + SPAN / 2);
             }
-            int cur = buf;  // buffer holding the current 32-neighbour chunk
-            const T* xin0 = a.x_in + col_of(slab, 0);
-            const T* xin1 = xin0 + SPAN / 2;
-            // integer mode: SWAR byte counters of +1 signs, p0 elements 0..3, p1 elements 4..7
-            // (<= 224 neighbours per fold; hub rows fold into wide counters)
-            uint32_t p0 = 0, p1 = 0, wide[E];
-            int folded = 0, in_bytes = 0;
-            bool wide_used = false;
-            bool fmode = cin == nullptr;
-            T acc[E];  // fp mode: the running sum
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = T(0);
-            auto unpack = [&](int e) -> uint32_t {
-                return __byte_perm(e < 4 ? p0 : p1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
-            };
-            for (int base = 0; base < deg; base += 32) {
-                const int cnt = min(32, deg - base);
-                int nxt = cur;
-                if (cin && base + 32 < deg) {  // hub rows: stage the next chunk while this one is summed
-                    nxt = cur == kD + 1 ? buf : kD + 1;
-                    __syncwarp();  // every lane is done with buffer nxt (the chunk before this one)
-                    stage_codes(s, sl, nxt, base + 32);
-                    // chunk 0 landed with the tile's group; later chunks: everything but the copy
-                    // just issued (the lookahead tiles' groups are older and complete with it)
-                    if (base > 0) cp_async_wait1();
-                    __syncwarp();
-                } else if (cin && base > 0) {
-                    cp_async_wait0();
-                    __syncwarp();
+            T nacc[E];
+            // Fast path (the saturated steady state): <= 32 neighbours, all on the box corners.
+            // Sign bytes are compressed three at a time (full adder: parity = weight 1,
+            // majority = weight 2) before the nibble spread into byte counters.
+            bool fast = false;
+            if (cin != nullptr && deg <= 32) {
+                const uint32_t* fb0 = &sm.flags[j][buf][0];
+                fast = !__any_sync(0xffffffffu, lane < deg && fb0[lane] != 0u);
+            }
+            if (fast) {
+                const uint8_t* cb = &sm.codes[j][buf][0][lane];
+                auto spread = [](uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; };
+                uint32_t q0 = 0, q1 = 0;  // +1 counts: byte e of q0 = element e, of q1 = element 4 + e
+                int k = 0;
+                for (; k + 3 <= deg; k += 3) {
+                    const uint32_t b0 = cb[32 * k], b1 = cb[32 * (k + 1)], b2 = cb[32 * (k + 2)];
+                    const uint32_t par = b0 ^ b1 ^ b2;
+                    const uint32_t maj = (b0 & b1) | (b2 & (b0 | b1));
+                    q0 += spread(par & 0xFu) + 2u * spread(maj & 0xFu);
+                    if constexpr (E == 8) q1 += spread(par >> 4) + 2u * spread(maj >> 4);
                 }
-                const uint8_t* cb = &sm.codes[j][cur][0][lane];  // neighbour k's sign byte for this lane: cb[32 k]
-                const uint32_t* fb = &sm.flags[j][cur][0];
-                cur = nxt;
-                if (!fmode) {
-                    const bool interior = __any_sync(0xffffffffu, lane < cnt && fb[lane] != 0u);
-                    if (!interior) {
-#pragma unroll 4
-                        for (int k = 0; k < cnt; ++k) {
-                            const uint32_t b = cb[32 * k];
-                            p0 += ((b & 0xFu) * 0x00204081u) & 0x01010101u;  // sign bit e -> byte e
-                            if constexpr (E == 8) p1 += ((b >> 4) * 0x00204081u) & 0x01010101u;
-                        }
-                        folded += cnt;
-                        in_bytes += cnt;
-                        if (in_bytes > 224) {  // hub rows: keep the byte counters from overflowing
-                            if (!wide_used) {
+                for (; k < deg; ++k) {
+                    const uint32_t b = cb[32 * k];
+                    q0 += spread(b & 0xFu);
+                    if constexpr (E == 8) q1 += spread(b >> 4);
+                }
 #pragma unroll
-                                for (int e = 0; e < E; ++e) wide[e] = 0;
-                                wide_used = true;
-                            }
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t c = __byte_perm(e < 4 ? q0 : q1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
+                    nacc[e] = -static_cast<T>(2 * static_cast<int>(c) - deg);
+                }
+            } else {
+                int cur = buf;  // buffer holding the current 32-neighbour chunk
+                const T* xin0 = a.x_in + col_of(slab, 0);
+                const T* xin1 = xin0 + SPAN / 2;
+                // integer mode: SWAR byte counters of +1 signs, p0 elements 0..3, p1 elements 4..7
+                // (<= 224 neighbours per fold; hub rows fold into wide counters)
+                uint32_t p0 = 0, p1 = 0, wide[E];
+                int folded = 0, in_bytes = 0;
+                bool wide_used = false;
+                bool fmode = cin == nullptr;
+                T acc[E];  // fp mode: the running sum
 #pragma unroll
-                            for (int e = 0; e < E; ++e) wide[e] += unpack(e);
-                            p0 = p1 = 0;
-                            in_bytes = 0;
-                        }
-                        continue;
+                for (int e = 0; e < E; ++e) acc[e] = T(0);
+                auto unpack = [&](int e) -> uint32_t {
+                    return __byte_perm(e < 4 ? p0 : p1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
+                };
+                for (int base = 0; base < deg; base += 32) {
+                    const int cnt = min(32, deg - base);
+                    int nxt = cur;
+                    if (cin && base + 32 < deg) {  // hub rows: stage the next chunk while this one is summed
+                        nxt = cur == kD + 1 ? buf : kD + 1;
+                        __syncwarp();  // every lane is done with buffer nxt (the chunk before this one)
+                        stage_codes(s, sl, nxt, base + 32);
+                        // chunk 0 landed with the tile's group; later chunks: everything but the copy
+                        // just issued (the lookahead tiles' groups are older and complete with it)
+                        if (base > 0) cp_async_wait1();
+                        __syncwarp();
+                    } else if (cin && base > 0) {
+                        cp_async_wait0();
+                        __syncwarp();
                     }
-                    fmode = true;  // exact partial sum so far: (+1 count) - (-1 count)
+                    const uint8_t* cb = &sm.codes[j][cur][0][lane];  // neighbour k's sign byte for this lane: cb[32 k]
+                    const uint32_t* fb = &sm.flags[j][cur][0];
+                    cur = nxt;
+                    if (!fmode) {
+                        const bool interior = __any_sync(0xffffffffu, lane < cnt && fb[lane] != 0u);
+                        if (!interior) {
+#pragma unroll 4
+                            for (int k = 0; k < cnt; ++k) {
+                                const uint32_t b = cb[32 * k];
+                                p0 += ((b & 0xFu) * 0x00204081u) & 0x01010101u;  // sign bit e -> byte e
+                                if constexpr (E == 8) p1 += ((b >> 4) * 0x00204081u) & 0x01010101u;
+                            }
+                            folded += cnt;
+                            in_bytes += cnt;
+                            if (in_bytes > 224) {  // hub rows: keep the byte counters from overflowing
+                                if (!wide_used) {
+#pragma unroll
+                                    for (int e = 0; e < E; ++e) wide[e] = 0;
+                                    wide_used = true;
+                                }
+#pragma unroll
+                                for (int e = 0; e < E; ++e) wide[e] += unpack(e);
+                                p0 = p1 = 0;
+                                in_bytes = 0;
+                            }
+                            continue;
+                        }
+                        fmode = true;  // exact partial sum so far: (+1 count) - (-1 count)
+#pragma unroll
+                        for (int e = 0; e < E; ++e)
+                            acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
+                    }
+                    // sequential fp adds; the neighbour index is only needed for interior neighbours
+                    for (int k = 0; k < cnt; k += kFNB) {
+                        T g[kFNB][E];
+                        uint32_t bq[kFNB];
+                        bool in[kFNB];
+#pragma unroll
+                        for (int q = 0; q < kFNB; ++q) {
+                            const int kk = k + q;
+                            const bool live = kk < cnt;
+                            in[q] = live && (cin == nullptr || fb[kk] != 0u);  // warp-uniform
+                            bq[q] = (live && cin) ? cb[32 * kk] : 0u;
+                            if (in[q]) {
+                                const int u =
+                                    coff >= 0 ? sm.col[s][coff + base + kk] : __ldg(a.col + sm.beg[s][j] + base + kk);
+                                const int64_t o = static_cast<int64_t>(u) * a.ld;
+                                ldg16(&g[q][0], xin0 + o);
+                                ldg16(&g[q][H], xin1 + o);
+                            }
+                        }
+                        bool all_in = true;
+#pragma unroll
+                        for (int q = 0; q < kFNB; ++q) all_in = all_in && (in[q] || k + q >= cnt);
+                        if (all_in) {  // before saturation: every neighbour gathered, plain adds
+#pragma unroll
+                            for (int q = 0; q < kFNB; ++q)
+                                if (k + q < cnt)
+#pragma unroll
+                                    for (int e = 0; e < E; ++e) acc[e] = radd(acc[e], g[q][e]);
+                            continue;
+                        }
+#pragma unroll
+                        for (int q = 0; q < kFNB; ++q) {
+                            if (k + q < cnt) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e)
+                                    acc[e] = radd(acc[e], in[q] ? g[q][e] : (((bq[q] >> e) & 1u) ? T(1) : T(-1)));
+                            }
+                        }
+                    }
+                }
+                // -acc, exact: -((count of +1) - (count of -1)); negated after the conversion so a zero
+                // sum is -0.0 exactly as -(+0.0) of the sequential sum
+                if (!fmode) {
 #pragma unroll
                     for (int e = 0; e < E; ++e)
-                        acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
+                        nacc[e] = -static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) nacc[e] = -acc[e];
                 }
-                // sequential fp adds; the neighbour index is only needed for interior neighbours
-                for (int k = 0; k < cnt; k += kFNB) {
-                    T g[kFNB][E];
-                    uint32_t bq[kFNB];
-                    bool in[kFNB];
-#pragma unroll
-                    for (int q = 0; q < kFNB; ++q) {
-                        const int kk = k + q;
-                        const bool live = kk < cnt;
-                        in[q] = live && (cin == nullptr || fb[kk] != 0u);  // warp-uniform
-                        bq[q] = (live && cin) ? cb[32 * kk] : 0u;
-                        if (in[q]) {
-                            const int u =
-                                coff >= 0 ? sm.col[s][coff + base + kk] : __ldg(a.col + sm.beg[s][j] + base + kk);
-                            const int64_t o = static_cast<int64_t>(u) * a.ld;
-                            ldg16(&g[q][0], xin0 + o);
-                            ldg16(&g[q][H], xin1 + o);
-                        }
-                    }
-                    bool all_in = true;
-#pragma unroll
-                    for (int q = 0; q < kFNB; ++q) all_in = all_in && (in[q] || k + q >= cnt);
-                    if (all_in) {  // before saturation: every neighbour gathered, plain adds
-#pragma unroll
-                        for (int q = 0; q < kFNB; ++q)
-                            if (k + q < cnt)
-#pragma unroll
-                                for (int e = 0; e < E; ++e) acc[e] = radd(acc[e], g[q][e]);
-                        continue;
-                    }
-#pragma unroll
-                    for (int q = 0; q < kFNB; ++q) {
-                        if (k + q < cnt) {
-#pragma unroll
-                            for (int e = 0; e < E; ++e)
-                                acc[e] = radd(acc[e], in[q] ? g[q][e] : (((bq[q] >> e) & 1u) ? T(1) : T(-1)));
-                        }
-                    }
-                }
-            }
-            // -acc, exact: -((count of +1) - (count of -1)); negated after the conversion so a zero
-            // sum is -0.0 exactly as -(+0.0) of the sequential sum
-            T nacc[E];
-            if (!fmode) {
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    nacc[e] = -static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) nacc[e] = -acc[e];
             }
 
             // ---- epilogue (ascent.cpp:66-77)
@@ -609,7 +680,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             } else if (own_ld) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) xv[e] = xg[e];
-            } else {
+            } else if constexpr (kXBox) {
                 ld16(&xv[0], &sm.x[s][j][16 * lane]);
                 ld16(&xv[H], &sm.x[s][j][512 + 16 * lane]);
             }

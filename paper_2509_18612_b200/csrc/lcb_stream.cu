@@ -240,6 +240,20 @@ constexpr int kClaim = LCB_STREAM_CLAIM;  // tiles per dynamic claim
 // always load their own stored x (the SMEM goes to deeper v staging)
 constexpr bool kXBox = LCB_STREAM_XBOX != 0;
 
+// every one of the E values finite: the products with zero are +-0 exactly then, NaN otherwise
+__device__ __forceinline__ bool finite_all(const float* r) {
+    float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) fma2(z0, z1, r[e], r[e + 1], 0.f, 0.f, z0, z1);
+    return z0 + z1 == 0.f;
+}
+__device__ __forceinline__ bool finite_all(const double* r) {
+    double z = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) z = fma(r[e], 0.0, z);
+    return z == 0.0;
+}
+
 struct StreamSmem {
     alignas(128) unsigned char x[kXBox ? kStages : 1][kXBox ? kR : 1][kXBox ? kSlab : 128];
     alignas(128) unsigned char v[kStages][kR][kSlab];
@@ -694,9 +708,14 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 // every element steps with the uniform alpha (the steady state)
 #pragma unroll
                 for (int e = 0; e < E; e += 2) pga_raw_neg2(&xv[e], &nacc[e], &vv[e], a.alpha_uniform, a.mu, dg, &raw[e]);
+                // finite check (ascent.cpp:70-72) folded: sum of raw * 0 is NaN iff some raw is not
+                // finite; the per-element mask only then
+                if (!finite_all(raw)) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) bad |= isfinite(raw[e]) ? 0u : 1u << e;
+                }
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    bad |= isfinite(raw[e]) ? 0u : 1u << e;                  // ascent.cpp:70-72
                     xo[e] = fmin(fmax(raw[e], T(-1)), T(1));                 // ascent.cpp:73 (raw finite)
                     if constexpr (EE) {
                         const T ch = fabs(xo[e] - xv[e]);

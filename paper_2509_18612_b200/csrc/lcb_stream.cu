@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -46,7 +47,7 @@ namespace lcb {
 namespace {
 
 #ifndef LCB_STREAM_R
-#define LCB_STREAM_R 16
+#define LCB_STREAM_R 23
 #endif
 constexpr int kR = LCB_STREAM_R;  // rows per tile = consumer warps per CTA
 constexpr int kThreadsS = 32 * (kR + 1);
@@ -90,21 +91,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) { mbar_arrive(smem_u32(bar)); }
 // the suspend-time hint parks a waiting warp in the barrier unit instead of re-issuing the probe
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
+        "}\n" ::"r"(bar),
         "r"(parity), "r"(1000000u)
         : "memory");
 }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait(smem_u32(bar), parity); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
@@ -127,6 +130,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -146,6 +155,12 @@ __device__ __forceinline__ void ld16(float* v, const void* smem) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
                  : "r"(smem_u32(smem)));
+}
+__device__ __forceinline__ void ld16(float* v, uint32_t a) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(a));
+}
+__device__ __forceinline__ void ld16(double* v, uint32_t a) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
 }
 __device__ __forceinline__ void ld16(double* v, const void* smem) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(smem_u32(smem)));
@@ -234,7 +249,7 @@ constexpr int kClaim = LCB_STREAM_CLAIM;  // tiles per dynamic claim
 #define LCB_STREAM_EXP 0  // timing experiments only (wrong results): 1 consumers idle, 2 no v box
 #endif
 #ifndef LCB_STREAM_XBOX
-#define LCB_STREAM_XBOX 1
+#define LCB_STREAM_XBOX 0
 #endif
 // 1: the producer stages the tile's x box when every row needs its stored x; 0: consumers
 // always load their own stored x (the SMEM goes to deeper v staging)
@@ -466,6 +481,16 @@ __global__ void __launch_bounds__(kThreadsS, 1)
     uint8_t* const cout = a.sgn_out;
     uint32_t* const fout = cout ? reinterpret_cast<uint32_t*>(cout + a.flag_off) : nullptr;
 
+    // 32-bit shared addresses of this warp's / lane's slots (buffer / stage offsets added per use)
+    const uint32_t sb = smem_u32(smem_raw);
+    const uint32_t a_codes = sb + static_cast<uint32_t>(offsetof(StreamSmem, codes)) + (j * kCB * 32 + lane) * 32u;
+    const uint32_t a_flags = sb + static_cast<uint32_t>(offsetof(StreamSmem, flags)) + (j * kCB * 32 + lane) * 4u;
+    const uint32_t a_own = sb + static_cast<uint32_t>(offsetof(StreamSmem, own)) + j * (kD + 1) * 32 + 4 * (lane & 7);
+    const uint32_t a_v = sb + static_cast<uint32_t>(offsetof(StreamSmem, v)) + j * kSlab + 16 * lane;
+    const uint32_t a_x = sb + static_cast<uint32_t>(offsetof(StreamSmem, x)) + j * kSlab + 16 * lane;
+    const uint32_t a_full = sb + static_cast<uint32_t>(offsetof(StreamSmem, full));
+    const uint32_t a_empty = sb + static_cast<uint32_t>(offsetof(StreamSmem, empty));
+
     // code lines + flags of neighbours [k0, k0 + 32) of the row in stage st -> buffer buf
     auto stage_codes = [&](int st, int sl, int buf, int k0) {
         const int row = sm.row[st][j];
@@ -476,13 +501,14 @@ __global__ void __launch_bounds__(kThreadsS, 1)
                 const int coff = sm.coff[st][j];
                 const int u = coff >= 0 ? sm.col[st][coff + k] : __ldg(a.col + sm.beg[st][j] + k);
                 const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(u);
-                cp_async16(&sm.codes[j][buf][lane][0], cin + line * 32u);
-                cp_async16(&sm.codes[j][buf][lane][16], cin + line * 32u + 16u);
-                cp_async4(&sm.flags[j][buf][lane], fin + line);
+                const uint32_t dc = a_codes + static_cast<uint32_t>(buf) * 1024u;
+                cp_async16(dc, cin + line * 32u);
+                cp_async16(dc + 16u, cin + line * 32u + 16u);
+                cp_async4(a_flags + static_cast<uint32_t>(buf) * 128u, fin + line);
             }
             if (k0 == 0 && lane >= 24 && a.xskip && sm.xfl[st][j] == 0) {  // own line, 4 bytes per lane
                 const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(row);
-                cp_async4(&sm.own[j][buf][4 * (lane - 24)], cin + line * 32u + 4u * (lane - 24));
+                cp_async4(a_own + static_cast<uint32_t>(buf) * 32u, cin + line * 32u + 4u * (lane - 24));
             }
         }
         cp_async_commit();
@@ -515,7 +541,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
         have[kD] = false;
         if (have[kD - 1]) {  // tile i + kD's stage has normally landed (the producer runs ahead)
             const int sn = (i + kD) % kStages;
-            mbar_wait(&sm.full[sn], ((i + kD) / kStages) & 1);
+            mbar_wait(a_full + 8u * static_cast<uint32_t>(sn), ((i + kD) / kStages) & 1);
             have[kD] = sm.slab[sn] >= 0;
         }
         if (have[kD])
@@ -695,11 +721,11 @@ __global__ void __launch_bounds__(kThreadsS, 1)
 #pragma unroll
                 for (int e = 0; e < E; ++e) xv[e] = xg[e];
             } else if constexpr (kXBox) {
-                ld16(&xv[0], &sm.x[s][j][16 * lane]);
-                ld16(&xv[H], &sm.x[s][j][512 + 16 * lane]);
+                ld16(&xv[0], a_x + static_cast<uint32_t>(s) * (kR * kSlab));
+                ld16(&xv[H], a_x + static_cast<uint32_t>(s) * (kR * kSlab) + 512u);
             }
-            ld16(&vv[0], &sm.v[s][j][16 * lane]);
-            ld16(&vv[H], &sm.v[s][j][512 + 16 * lane]);
+            ld16(&vv[0], a_v + static_cast<uint32_t>(s) * (kR * kSlab));
+            ld16(&vv[H], a_v + static_cast<uint32_t>(s) * (kR * kSlab) + 512u);
             const T dg = static_cast<T>(deg);
             T raw[E], xo[E];
             uint32_t bad = 0, sign = 0;
@@ -782,7 +808,7 @@ __global__ void __launch_bounds__(kThreadsS, 1)
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        if (lane == 0) mbar_arrive(a_empty + 8u * static_cast<uint32_t>(s));
 #pragma unroll
         for (int d = 0; d < kD; ++d) have[d] = have[d + 1];
     }

@@ -1,0 +1,8 @@
+for v in default s5 r21 r23 xb; do
+if [ $v = default ]; then unset LCB_LIB_PATH; else export LCB_LIB_PATH=build_variants/$v.so; fi
+python tools/kbench.py --graph er --n 1000000 --B 512 --T 500 --quco-only --tag "c4 $v" 2>&1 | tail -1
+python tools/kbench.py --graph ba --n 100000 --B 256 --T 500 --quco-only --tag "c5 $v" 2>&1 | tail -1
+done
+unset LCB_LIB_PATH
+python tools/kbench.py --graph er --n 1000000 --B 512 --T 20 --quco-only --tag "c4 T20" 2>&1 | tail -1
+timeout 1500 python -m pytest tests/test_gpu_stream.py tests/test_gpu_kernels_fp32.py -q -x --timeout 900 2>&1 | tail -1

@@ -137,6 +137,29 @@ def test_ascent_trace_counts_every_step():  # test_ascent.cpp:208-223
     assert tr.shape == (7, 2)
 
 
+@pytest.mark.parametrize("l,prec", [(1, LCB_FP64), (2, LCB_FP64), (2, LCB_FP32)])
+def test_ascent_trace_values_vs_oracle(l, prec):
+    """Objective trace values (ascent.cpp:78-88: x'Lx summed over the lift columns after
+    every step) against the oracle's sequential fp64 sums: the device reduction order
+    differs, so equal to 1e-12 relative in fp64 (the states themselves bitwise), 1e-5 in fp32."""
+    cg = O.generate_er(1500, 0.006, 5)
+    g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+    rng = np.random.default_rng(l)
+    B, T = 12, 25
+    x = rng.uniform(-0.3, 0.3, B * l * cg.n)
+    s = lc.DenseState(cg.n, l, B)
+    s.values[:] = x
+    seen = np.full((T, B), np.nan)
+    lc.ascend(g, s, lc.AscentParams(0.05, T, 0.9), precision=prec,
+              trace=lambda it, m, obj: seen.__setitem__((it, m), obj))
+    want_x, want = O.ascend(cg, x, l, B, 0.05, T, 0.9, False, trace=True)
+    assert not np.isnan(seen).any()
+    tol = 1e-12 if prec == LCB_FP64 else 1e-5
+    assert np.max(np.abs(seen - want) / np.maximum(np.abs(want), 1.0)) <= tol
+    if prec == LCB_FP64:
+        assert np.array_equal(s.values, want_x)
+
+
 # --------------------------------------------------------------- objectives / epilogue
 def test_laplacian_apply():
     g = lc.Graph(2, [(0, 1)])

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define LCB_ABI_VERSION 2
+#define LCB_ABI_VERSION 3
 
 enum lcb_status {
     LCB_OK = 0,
@@ -29,7 +29,8 @@ enum lcb_status {
     LCB_SHAPE = 2,
     LCB_NUMERIC = 3,
     LCB_CUDA = 4,
-    LCB_ERROR = 5
+    LCB_ERROR = 5,
+    LCB_PARSE = 6 /* ParseError (graph.cpp:145-165) */
 };
 
 /* Arithmetic of the iterate.  FP64 reproduces the reference (fp64, no FMA,
@@ -67,6 +68,15 @@ int lcb_graph_create(uint32_t n, const int64_t* offsets, const uint32_t* adjacen
  * eu / ev: m endpoints (duplicates and either orientation allowed). */
 int lcb_graph_from_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t m, int device,
                          lcb_graph** out);
+/* parse_edge_list(text) (graph.hpp:63-64, graph.cpp:136-172) on the device: the Gset /
+ * edge-list text ("n m" header, then "u v [w]" lines with 1-based ids; '%' / '#' comments
+ * and blank lines skipped) parsed line-parallel, then Graph(n, edges) built as in
+ * lcb_graph_from_edges.  LCB_PARSE with the reference's message ("line <k>: expected
+ * header \"n m\"", "... expected edge \"u v [w]\"", "... node id out of range [1, n]",
+ * "empty input: ..."), LCB_VALIDATION for a self-loop ("line <k>: self-loop at node <u>").
+ * saw_weights (optional) = 1 when an edge line carried a weight (the reference warns that
+ * weights are ignored). */
+int lcb_graph_parse(const char* text, int64_t len, int device, lcb_graph** out, int* saw_weights);
 /* The CSR of a graph handle (Graph::offsets / adjacency, graph.hpp:52-57):
  * offsets [n+1], adjacency [2m] (either may be null). */
 int lcb_graph_csr(const lcb_graph* g, int64_t* offsets, uint32_t* adjacency);

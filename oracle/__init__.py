@@ -126,6 +126,7 @@ def _load_ref():
         "ref_last_error": (C.c_char_p, []),
         "ref_graph_new": (C.c_int, [u32, P, P, i64, C.POINTER(P)]),
         "ref_graph_load": (C.c_int, [C.c_char_p, C.POINTER(P)]),
+        "ref_graph_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(P)]),
         "ref_graph_er": (C.c_int, [u32, f64, u64, C.POINTER(P)]),
         "ref_graph_free": (None, [P]),
         "ref_graph_shape": (None, [P, P, P, P]),
@@ -360,6 +361,16 @@ class RefGraph:
     def from_csr(cls, g: CSR):
         eu, ev = g.edges()
         return cls.from_edges(g.n, eu, ev)
+
+    @classmethod
+    def parse(cls, text: bytes):
+        """The reference's parse_edge_list(text); OracleError(status 6 = ParseError, 1 =
+        ValidationError) with the reference's message."""
+        h = C.c_void_p()
+        s = ref.ref_graph_parse(text, len(text), C.byref(h))
+        if s != 0:
+            raise OracleError(s, ref.ref_last_error().decode())
+        return cls(h.value)
 
     @classmethod
     def er(cls, n, p, seed):

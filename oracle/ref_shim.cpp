@@ -46,7 +46,7 @@ int guarded(F&& f) {
         return 1;
     } catch (const ParseError& e) {
         g_err = e.what();
-        return 1;
+        return 6;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 5;
@@ -112,6 +112,11 @@ int ref_graph_new(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t ne
 
 int ref_graph_load(const char* path, void** out) {
     return guarded([&] { *out = new Graph(load_graph_file(path)); });
+}
+
+// parse_edge_list(text) (graph.cpp:136-172, 174-177)
+int ref_graph_parse(const char* text, int64_t len, void** out) {
+    return guarded([&] { *out = new Graph(parse_edge_list(std::string(text, static_cast<std::size_t>(len)))); });
 }
 
 int ref_graph_er(uint32_t n, double p, uint64_t seed, void** out) {

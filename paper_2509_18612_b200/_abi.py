@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("LCB_LIB_PATH") or os.path.join(HERE, "libliftcut_b200
 P = C.c_void_p
 i64, u64, u32, i32, f64 = C.c_int64, C.c_uint64, C.c_uint32, C.c_int32, C.c_double
 
-LCB_OK, LCB_VALIDATION, LCB_SHAPE, LCB_NUMERIC, LCB_CUDA, LCB_ERROR = range(6)
+LCB_OK, LCB_VALIDATION, LCB_SHAPE, LCB_NUMERIC, LCB_CUDA, LCB_ERROR, LCB_PARSE = range(7)
 LCB_FP64, LCB_FP32 = 0, 1
 
 
@@ -82,6 +82,7 @@ SIGNATURES = {
     "lcb_round": (C.c_int, [C.c_int, P, i64, i32, i64, i32, P]),
     "lcb_brute_force_maxcut": (C.c_int, [P, i32, P, P, P]),
     "lcb_graph_from_edges": (C.c_int, [u32, P, P, i64, C.c_int, C.POINTER(P)]),
+    "lcb_graph_parse": (C.c_int, [C.c_char_p, i64, C.c_int, C.POINTER(P), C.POINTER(C.c_int)]),
     "lcb_graph_csr": (C.c_int, [P, P, P]),
     "lcb_dui_init": (C.c_int, [P, u64, P]),
     "lcb_idi_init": (C.c_int, [P, f64, u64, P]),
@@ -117,7 +118,7 @@ def lib():
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
-        if L.lcb_abi_version() != 2:
+        if L.lcb_abi_version() != 3:
             raise RuntimeError("libliftcut_b200.so ABI mismatch")
         _lib = L
     return _lib

@@ -113,11 +113,24 @@ IngestResult ingest_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, in
                                               std::to_string(b) + ") with n=" + std::to_string(n)};
         throw Failure{LCB_VALIDATION, "self-loop at node " + std::to_string(a)};
     }
+    return ingest_edges_device(n, du.p, dv.p, m, s);
+}
+
+IngestResult ingest_edges_device(uint32_t n, const uint32_t* du, const uint32_t* dv, int64_t m, cudaStream_t s) {
+    if (n == 0) throw Failure{LCB_VALIDATION, "graph must have at least one node"};
+    IngestResult res;
+    res.off.assign(static_cast<size_t>(n) + 1, 0);
+    const unsigned grid = 148 * 8;
+    if (m == 0) {
+        cuda_check(cudaMalloc(&res.col, sizeof(int) * 4), "cudaMalloc(col)");  // + K1s bulk-copy pad
+        res.nnz = 0;
+        return res;
+    }
     const int bits = key_bits(n);
     // normalise, sort, unique
     DevMem<uint64_t> k0(static_cast<size_t>(m)), k1(static_cast<size_t>(m));
     count_launch();
-    k_edge_keys<<<grid, 256, 0, s>>>(du.p, dv.p, m, k0.p);
+    k_edge_keys<<<grid, 256, 0, s>>>(du, dv, m, k0.p);
     size_t tb_sort = 0, tb_uniq = 0, tb_sort2 = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, k0.p, k1.p, m, 0, bits, s);
     cub::DeviceSelect::Unique(nullptr, tb_uniq, k1.p, k0.p, static_cast<int64_t*>(nullptr), m, s);

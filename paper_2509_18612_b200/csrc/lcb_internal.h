@@ -280,6 +280,11 @@ struct IngestResult {
     int64_t nnz = 0;
 };
 IngestResult ingest_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int64_t m, cudaStream_t s);
+// the same from device endpoint arrays already validated (ids < n, no self-loops)
+IngestResult ingest_edges_device(uint32_t n, const uint32_t* du, const uint32_t* dv, int64_t m, cudaStream_t s);
+// parse_edge_list (graph.cpp:136-172) of a whole text on the device, then ingest; n of the
+// header out, saw_weights = some edge line carried a weight (the reference warns)
+IngestResult parse_edge_text(const char* text, int64_t len, uint32_t& n_out, bool& saw_weights, cudaStream_t s);
 
 // process-wide counters (bench evidence: launches and host<->device bytes)
 void count_launch(int k = 1);

@@ -2161,6 +2161,34 @@ int lcb_graph_from_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int
     });
 }
 
+int lcb_graph_parse(const char* text, int64_t len, int device, lcb_graph** out, int* saw_weights) {
+    return guard([&] {
+        if (!out || (len > 0 && !text)) fail(LCB_VALIDATION, "null argument");
+        DeviceScope ds(device);
+        uint32_t n = 0;
+        bool weights = false;
+        IngestResult r = parse_edge_text(text, len, n, weights, 0);
+        auto h = std::make_unique<lcb_graph>();
+        try {
+            std::vector<uint32_t> hadj;
+            if (n <= static_cast<uint32_t>(kResidentMaxRows) && r.nnz) {
+                hadj.resize(static_cast<size_t>(r.nnz));
+                d2h(hadj.data(), r.col, sizeof(int) * static_cast<size_t>(r.nnz), 0);
+                CK(cudaStreamSynchronize(0));
+            }
+            int* col = r.col;
+            r.col = nullptr;
+            build_graph(h->g, n, r.off.data(), hadj.empty() ? nullptr : hadj.data(), device, col);
+        } catch (...) {
+            if (r.col) cudaFree(r.col);
+            free_graph(h->g);
+            throw;
+        }
+        if (saw_weights) *saw_weights = weights ? 1 : 0;
+        *out = h.release();
+    });
+}
+
 int lcb_graph_csr(const lcb_graph* g, int64_t* offsets, uint32_t* adjacency) {
     return guard([&] {
         if (!g) fail(LCB_VALIDATION, "null graph");

@@ -17,6 +17,8 @@ import ctypes as C
 import enum
 import math
 import os
+import re
+import warnings
 from dataclasses import dataclass, field, replace
 from typing import Callable, Optional
 
@@ -59,6 +61,8 @@ def _raise(status: int):
         raise ShapeError(msg)
     if status == _abi.LCB_NUMERIC:
         raise NumericError(msg)
+    if status == _abi.LCB_PARSE:
+        raise ParseError(msg)
     raise Error(msg or f"liftcut_b200 status {status}")
 
 
@@ -329,27 +333,47 @@ class Graph:
         return y
 
 
+_LL_MAX = (1 << 63) - 1
+_INT_RE = re.compile(r"[ \t\n\v\f\r]*([+-]?)([0-9]+)")
+_NUM_RE = re.compile(r"[ \t\n\v\f\r]*[+-]?(?:[0-9]|\.[0-9])")
+
+
+def _read_ll(s: str, pos: int):
+    """istream >> long long: skip isspace, optional sign, digits; None on failure/overflow."""
+    mt = _INT_RE.match(s, pos)
+    if not mt:
+        return None, pos
+    v = int(mt.group(2))
+    if (mt.group(1) == "-" and v > _LL_MAX + 1) or (mt.group(1) != "-" and v > _LL_MAX):
+        return None, pos
+    return (-v if mt.group(1) == "-" else v), mt.end()
+
+
 def parse_edge_list(text: str) -> Graph:
-    """Gset text (graph.cpp:136-172)."""
+    """Gset text (graph.cpp:136-172): is_comment_or_blank skips only ' ', '\t', '\r' before
+    '%' / '#'; numbers follow the istream rules for long long."""
     n = m = -1
     us, vs = [], []
-    for line_no, line in enumerate(text.splitlines(), 1):
-        s = line.strip()
+    saw_weights = False
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()  # std::getline: a trailing newline ends the last line
+    for line_no, line in enumerate(lines, 1):
+        s = line.lstrip(" \t\r")
         if not s or s[0] in "%#":
             continue
-        tok = s.split()
         if n < 0:
-            try:
-                n, m = int(tok[0]), int(tok[1])
-            except (ValueError, IndexError):
-                raise ParseError(f'line {line_no}: expected header "n m"')
-            if n <= 0 or m < 0:
+            n, p = _read_ll(line, 0)
+            m, p = _read_ll(line, p) if n is not None else (None, p)
+            if n is None or m is None or n <= 0 or m < 0:
                 raise ParseError(f'line {line_no}: expected header "n m"')
             continue
-        try:
-            u, v = int(tok[0]), int(tok[1])
-        except (ValueError, IndexError):
+        u, p = _read_ll(line, 0)
+        v, p = _read_ll(line, p) if u is not None else (None, p)
+        if u is None or v is None:
             raise ParseError(f'line {line_no}: expected edge "u v [w]"')
+        if _NUM_RE.match(line, p):
+            saw_weights = True
         if u < 1 or u > n or v < 1 or v > n:
             raise ParseError(f"line {line_no}: node id out of range [1, {n}]")
         if u == v:
@@ -358,6 +382,8 @@ def parse_edge_list(text: str) -> Graph:
         vs.append(v - 1)
     if n < 0:
         raise ParseError('empty input: missing "n m" header')
+    if saw_weights:
+        warnings.warn("edge weights present in input are ignored (unweighted MaxCut)")
     return Graph(n, np.stack([np.array(us, dtype=np.int64), np.array(vs, dtype=np.int64)], 1))
 
 
@@ -368,19 +394,58 @@ def load_graph_file(path: str) -> Graph:
             text = f.read()
     except OSError:
         raise ParseError(f"cannot open graph file: {path}")
-    lines = [ln for ln in text.splitlines() if ln.strip() and ln.strip()[0] not in "%#"]
+    lines = [ln for ln in text.split("\n") if ln.lstrip(" \t\r") and ln.lstrip(" \t\r")[0] not in "%#"]
     if not lines:
         raise ParseError('empty input: missing "n m" header')
     try:
-        n = int(lines[0].split()[0])
+        n, m = (int(t) for t in lines[0].split())
         body = np.array(" ".join(lines[1:]).split(), dtype=np.int64)
         ncol = len(lines[1].split()) if len(lines) > 1 else 2
-        if ncol not in (2, 3) or any(len(ln.split()) != ncol for ln in lines[1:4]):
+        if ncol not in (2, 3) or body.size != ncol * (len(lines) - 1) or n <= 0 or m < 0:
             raise ValueError
         e = body.reshape(-1, ncol)[:, :2] - 1
-    except ValueError:
+        if len(e) and (e.min() < 0 or e.max() >= n or (e[:, 0] == e[:, 1]).any()):
+            raise ValueError  # the line-by-line parser reports the reference's error
+    except (ValueError, OverflowError):
         return parse_edge_list(text)
+    if ncol == 3:
+        warnings.warn("edge weights present in input are ignored (unweighted MaxCut)")
     return Graph(n, e)
+
+
+def parse_edge_list_device(text, device: Optional[int] = None) -> Graph:
+    """parse_edge_list (graph.cpp:136-172) on the GPU (lcb_graph_parse): line-parallel
+    parse, then the device Graph(n, edges) build; same CSR, errors and messages as the
+    reference.  A weight column warns like the reference (graph.cpp:168-169)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    dev = default_device() if device is None else device
+    h = C.c_void_p()
+    w = C.c_int(0)
+    _check(_abi.lib().lcb_graph_parse(data, len(data), dev, C.byref(h), C.byref(w)))
+    if w.value:
+        warnings.warn("edge weights present in input are ignored (unweighted MaxCut)")
+    n = C.c_uint32()
+    m = C.c_int64()
+    _abi.lib().lcb_graph_info(h, C.byref(n), C.byref(m), None)
+    off = np.zeros(int(n.value) + 1, dtype=np.int64)
+    adj = np.zeros(max(2 * m.value, 1), dtype=np.uint32)
+    st = _abi.lib().lcb_graph_csr(h, _ptr(off), _ptr(adj))
+    if st != 0:
+        _abi.lib().lcb_graph_destroy(h)
+        _check(st)
+    g = Graph(int(n.value), _csr=(int(n.value), off, adj[: 2 * m.value].copy()))
+    g._handles[dev] = h
+    return g
+
+
+def load_graph_file_device(path: str, device: Optional[int] = None) -> Graph:
+    """load_graph_file (graph.cpp:179-183) with the text parsed on the GPU."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise ParseError(f"cannot open graph file: {path}")
+    return parse_edge_list_device(data, device)
 
 
 def serialize_edge_list(g: Graph) -> str:

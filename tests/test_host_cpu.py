@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
     assert set(syms) == set(_abi.SIGNATURES), set(syms) ^ set(_abi.SIGNATURES)
-    assert _abi.lib().lcb_abi_version() == 2
+    assert _abi.lib().lcb_abi_version() == 3
 
 
 def test_struct_layouts_match_the_c_header():

@@ -22,6 +22,7 @@ inline void check(int status) {
         case LCB_VALIDATION: throw ValidationError(msg);
         case LCB_SHAPE: throw ShapeError(msg);
         case LCB_NUMERIC: throw NumericError(msg);
+        case LCB_PARSE: throw ParseError(msg);
         default: throw Error(msg);
     }
 }

@@ -98,6 +98,20 @@ int lcb_ascend(const lcb_graph* g, double* values, int64_t n, int32_t l, int64_t
                double* trace, int64_t* err_iter, int64_t* err_member);
 
 /* ---- objectives (objectives.hpp:25,47,50; solver.cpp:125-138) --------------- */
+/* Row-sharded ascend (north star 5; SURVEY 8e "row-sharding of A" for graphs beyond one
+ * HBM): the same result as lcb_ascend on the whole graph, with rank q holding only the CSR
+ * rows [row_begin, row_end) -- offsets [rows+1] starting at 0, adjacency with GLOBAL ids --
+ * and its slice values [B][l][rows] of the DenseState (in/out).  The ranks' ranges must
+ * partition [0, n) in rank order.  Every rank keeps the whole iterate; per iteration the
+ * new rows are all-gathered (NCCL grouped broadcasts, or the loopback) and, with early
+ * exit, the members' exit bits are OR-reduced, so the exit test sees the whole member
+ * (ascent.cpp:74-75, 91-93).  comm = NULL: one rank owning [0, n).  fp64 is bit-exact with
+ * the reference's ascend on the whole graph. */
+int lcb_ascend_rows(lcb_comm* comm, uint32_t n, int64_t row_begin, int64_t row_end, const int64_t* offsets,
+                    const uint32_t* adjacency, double* values, int32_t l, int64_t B, double alpha, int64_t iterations,
+                    double momentum, int32_t early_exit, int32_t precision, int device, int64_t* err_iter,
+                    int64_t* err_member);
+
 /* cut_value for `count` assignments z[count][n]; LCB_VALIDATION if an entry > 1. */
 int lcb_cut_values(const lcb_graph* g, const uint8_t* z, int64_t count, int64_t* cuts);
 /* Round every member of a [B][l][n] batch (round_unlifted when lifted == 0,

@@ -77,6 +77,7 @@ SIGNATURES = {
     "lcb_graph_info": (C.c_int, [P, P, P, P]),
     "lcb_laplacian_apply": (C.c_int, [P, P, P, i64, i32]),
     "lcb_ascend": (C.c_int, [P, P, i64, i32, i64, f64, i64, f64, i32, i32, P, P, P]),
+    "lcb_ascend_rows": (C.c_int, [P, u32, i64, i64, P, P, P, i32, i64, f64, i64, f64, i32, i32, C.c_int, P, P]),
     "lcb_cut_values": (C.c_int, [P, P, i64, P]),
     "lcb_round_cut_batch": (C.c_int, [P, P, i32, i64, i32, P, P, P, P]),
     "lcb_round": (C.c_int, [C.c_int, P, i64, i32, i64, i32, P]),

@@ -434,6 +434,30 @@ void launch_reduce_rows(const void* rows, int nrows, size_t count, int bytes, bo
     }
 }
 
+// per-member bit flags <-> one 0/1 word array per bit (an OR across ranks is then a MAX)
+__global__ void k_bits_split(const uint32_t* f, int count, int nbits, uint32_t* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        for (int k = 0; k < nbits; ++k) out[static_cast<size_t>(k) * count + i] = (f[i] >> k) & 1u;
+}
+__global__ void k_bits_merge(const uint32_t* in, int count, int nbits, uint32_t* f) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int k = 0; k < nbits; ++k) v |= (in[static_cast<size_t>(k) * count + i] ? 1u : 0u) << k;
+        f[i] = v;
+    }
+}
+
+void launch_bits_split(const uint32_t* f, int count, int nbits, uint32_t* out, cudaStream_t s) {
+    if (count <= 0) return;
+    count_launch();
+    k_bits_split<<<std::min((count + 255) / 256, 1024), 256, 0, s>>>(f, count, nbits, out);
+}
+void launch_bits_merge(const uint32_t* in, int count, int nbits, uint32_t* f, cudaStream_t s) {
+    if (count <= 0) return;
+    count_launch();
+    k_bits_merge<<<std::min((count + 255) / 256, 1024), 256, 0, s>>>(in, count, nbits, f);
+}
+
 template void launch_transpose_in<float>(const double*, float*, int, int, int64_t, cudaStream_t);
 template void launch_transpose_in<double>(const double*, double*, int, int, int64_t, cudaStream_t);
 template void launch_transpose_out<float>(const float*, double*, int, int, int64_t, cudaStream_t);

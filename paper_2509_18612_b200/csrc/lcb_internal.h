@@ -195,6 +195,9 @@ void launch_xcode_fill(T* X, int64_t ld, int n, const uint8_t* codes, int64_t fl
 
 template <typename T>
 void launch_transpose_in(const double* src, T* dst, int n, int W, int64_t ld, cudaStream_t s);
+// per-member flag words <-> nbits arrays of 0/1 words (OR across ranks as a MAX allreduce)
+void launch_bits_split(const uint32_t* f, int count, int nbits, uint32_t* out, cudaStream_t s);
+void launch_bits_merge(const uint32_t* in, int count, int nbits, uint32_t* f, cudaStream_t s);
 template <typename T>
 void launch_transpose_out(const T* src, double* dst, int n, int W, int64_t ld, cudaStream_t s);
 

@@ -560,6 +560,10 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    // row-sharded ascent (all-gather of row ranges as grouped broadcasts)
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 NcclApi& nccl() {
@@ -576,6 +580,9 @@ NcclApi& nccl() {
         a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
         a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
         a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(h, "ncclBroadcast"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
         a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy && a.GetErrorString;
         if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
         return a;
@@ -690,6 +697,54 @@ void comm_allreduce(lcb_comm* c, void* buf, size_t count, int bytes, bool is_max
     CK(cudaStreamSynchronize(st));
     g.barrier();  // every rank has read every slot before any slot is rewritten
 }
+
+// All-gather of row ranges of a node-major buffer: rank q owns rows [range[2q], range[2q+1])
+// of `base` (row_bytes each) and every rank ends with every range.  NCCL: one broadcast per
+// root inside a group; loopback: device staging + host barriers.
+void comm_allgather_rows(lcb_comm* c, void* base, size_t row_bytes, const std::vector<int64_t>& range,
+                         cudaStream_t st) {
+    if (!comm_active(c)) return;
+    char* b = static_cast<char*>(base);
+    if (c->comm) {
+        if (!nccl().Broadcast || !nccl().GroupStart || !nccl().GroupEnd)
+            fail(LCB_CUDA, "libnccl.so.2 lacks ncclBroadcast / ncclGroupStart / ncclGroupEnd");
+        nccl_check(nccl().GroupStart(), "ncclGroupStart");
+        for (int q = 0; q < c->nranks; ++q) {
+            const int64_t r0 = range[static_cast<size_t>(2 * q)], r1 = range[static_cast<size_t>(2 * q + 1)];
+            if (r1 > r0) {
+                char* p = b + static_cast<size_t>(r0) * row_bytes;
+                nccl_check(nccl().Broadcast(p, p, static_cast<size_t>(r1 - r0) * row_bytes, ncclUint8, q, c->comm, st),
+                           "ncclBroadcast(rows)");
+            }
+        }
+        nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+        return;
+    }
+    LoopGroup& g = *c->loop;
+    const size_t r = static_cast<size_t>(c->rank);
+    const int64_t r0 = range[2 * r], r1 = range[2 * r + 1];
+    const size_t nb = static_cast<size_t>(r1 - r0) * row_bytes;
+    if (g.cap[r] < nb) {
+        if (g.slot[r]) cudaFree(g.slot[r]);
+        g.slot[r] = nullptr;
+        g.cap[r] = 0;
+        CK(cudaMalloc(&g.slot[r], nb));
+        g.cap[r] = nb;
+        g.dev[r] = c->device;
+    }
+    if (nb) CK(cudaMemcpyAsync(g.slot[r], b + static_cast<size_t>(r0) * row_bytes, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    g.barrier();
+    for (int q = 0; q < g.nranks; ++q) {
+        if (q == c->rank) continue;
+        const int64_t q0 = range[static_cast<size_t>(2 * q)], q1 = range[static_cast<size_t>(2 * q + 1)];
+        if (q1 > q0)
+            CK(cudaMemcpyPeerAsync(b + static_cast<size_t>(q0) * row_bytes, c->device, g.slot[static_cast<size_t>(q)],
+                                   g.dev[static_cast<size_t>(q)], static_cast<size_t>(q1 - q0) * row_bytes, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    g.barrier();
+}
 }  // namespace lcb
 
 namespace lcb {
@@ -719,6 +774,9 @@ struct Work {
     DBuf<uint16_t> dplanes;      // dense path: 2 x 3 bf16 planes + K-step flags
     DBuf<float> dpartial;        // dense path: split-K partial sums of the tail tiles
     DBuf<uint32_t> win, recenter, pbest, gbest, carry, scratch_bits;
+    DBuf<uint32_t> orbits;       // row-sharded ascent: early-exit bits, one array per bit
+    DBuf<int> rs_row_ptr, rs_col, rs_order;  // row-sharded ascent: this rank's rows, global ids
+    DBuf<T> rs_deg;
     DBuf<uint64_t> bf;           // exhaustive scan: masks, upper masks, degrees, block records
     unsigned long long* h_keys = nullptr;  // pinned
     uint32_t* h_flags = nullptr;
@@ -2056,6 +2114,161 @@ void ascend_host(const DevGraph& g, double* values, int64_t n, int l, int64_t B,
     }
 }
 
+// Row-sharded ascend (north star 5: graphs whose adjacency does not fit one
+// HBM).  Rank q holds the CSR rows [r0_q, r1_q) (global column ids) and its slice
+// [B][l][r1_q - r0_q] of the state; the ranges partition [0, n).  Every rank keeps the
+// whole iterate X [n][ld] (double-buffered) and its own rows of V.  Per iteration: K1 over
+// the local rows (the reference's CSR-order sums, graph.cpp:116-121, so fp64 stays
+// bit-exact with ascend on the whole graph), the early-exit bits OR-reduced across ranks
+// (a MAX over one 0/1 array per bit), then an all-gather of the new rows.
+template <class T>
+void ascend_rows_host(lcb_comm* comm, uint32_t n, int64_t r0, int64_t r1, const int64_t* off, const uint32_t* adj,
+                      double* values, int l, int64_t B, double alpha, int64_t iters, double mu, bool ee,
+                      int device, int64_t* err_it, int64_t* err_m) {
+    if (!(alpha > 0.0)) fail(LCB_VALIDATION, "ascent: alpha must be > 0");
+    if (iters < 1) fail(LCB_VALIDATION, "ascent: iterations must be >= 1");
+    if (!(mu >= 0.0 && mu < 1.0)) fail(LCB_VALIDATION, "ascent: momentum must lie in [0, 1)");
+    if (l < 1 || B < 1) fail(LCB_VALIDATION, "DenseState: n, l, B must all be >= 1");
+    if (n == 0 || r0 < 0 || r1 < r0 || r1 > static_cast<int64_t>(n)) fail(LCB_VALIDATION, "row range outside [0, n)");
+    const int64_t rows = r1 - r0;
+    if (off[0] != 0) fail(LCB_VALIDATION, "offsets[0] must be 0");
+    for (int64_t i = 0; i < rows; ++i)
+        if (off[i + 1] < off[i]) fail(LCB_VALIDATION, "offsets must be non-decreasing");
+    const int64_t nnz = off[rows];
+    if (nnz > std::numeric_limits<int>::max()) fail(LCB_VALIDATION, "row range exceeds 2^31 adjacency entries");
+    for (int64_t k = 0; k < nnz; ++k)
+        if (adj[k] >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
+    const int64_t W64 = B * l;
+    if (W64 > (1 << 26)) fail(LCB_VALIDATION, "batch too wide");
+    const int W = static_cast<int>(W64);
+    const int members = static_cast<int>(B);
+    DeviceScope ds(device);
+    PooledWork<T> pw(device);
+    Work<T>& w = *pw;
+    w.shape(static_cast<int>(n), W);
+    // every rank's range, checked to partition [0, n)
+    const int nr = comm_active(comm) ? comm->nranks : 1, me = comm_active(comm) ? comm->rank : 0;
+    std::vector<int64_t> range(static_cast<size_t>(2 * nr), 0);
+    range[static_cast<size_t>(2 * me)] = r0;
+    range[static_cast<size_t>(2 * me + 1)] = r1;
+    if (nr > 1) {
+        unsigned long long* dr = w.keys.ensure(static_cast<size_t>(2 * nr));
+        std::vector<unsigned long long> hr(range.begin(), range.end());
+        h2d(dr, hr.data(), sizeof(unsigned long long) * hr.size(), w.st);
+        comm_allreduce(comm, dr, hr.size(), 8, true, w.st, "allreduce(row ranges)");
+        d2h(hr.data(), dr, sizeof(unsigned long long) * hr.size(), w.st);
+        CK(cudaStreamSynchronize(w.st));
+        for (size_t i = 0; i < hr.size(); ++i) range[i] = static_cast<int64_t>(hr[i]);
+    }
+    for (int q = 0; q < nr; ++q)
+        if (range[static_cast<size_t>(2 * q)] != (q ? range[static_cast<size_t>(2 * q - 1)] : 0))
+            fail(LCB_VALIDATION, "row ranges must partition [0, n) in rank order");
+    if (range[static_cast<size_t>(2 * nr - 1)] != static_cast<int64_t>(n))
+        fail(LCB_VALIDATION, "row ranges must partition [0, n) in rank order");
+    // this rank's rows at their global indices: row_ptr / deg hold entries r0 .. r1 only
+    int* rp = w.rs_row_ptr.ensure(static_cast<size_t>(n) + 1);
+    T* dg = w.rs_deg.ensure(static_cast<size_t>(n));
+    int* col = w.rs_col.ensure(static_cast<size_t>(nnz) + 4);
+    int* ord = w.rs_order.ensure(static_cast<size_t>(std::max<int64_t>(rows, 1)));
+    {
+        std::vector<int> hrp(static_cast<size_t>(rows) + 1), hord(static_cast<size_t>(rows));
+        std::vector<T> hdg(static_cast<size_t>(rows));
+        for (int64_t i = 0; i <= rows; ++i) hrp[static_cast<size_t>(i)] = static_cast<int>(off[i]);
+        for (int64_t i = 0; i < rows; ++i) {
+            hord[static_cast<size_t>(i)] = static_cast<int>(r0 + i);
+            hdg[static_cast<size_t>(i)] = static_cast<T>(off[i + 1] - off[i]);
+        }
+        h2d(rp + r0, hrp.data(), sizeof(int) * hrp.size(), w.st);
+        if (rows) {
+            h2d(dg + r0, hdg.data(), sizeof(T) * hdg.size(), w.st);
+            h2d(ord, hord.data(), sizeof(int) * hord.size(), w.st);
+        }
+        if (nnz) h2d(col, adj, sizeof(int) * static_cast<size_t>(nnz), w.st);
+        CK(cudaStreamSynchronize(w.st));  // the host vectors go out of scope
+    }
+    // the local slice in, then every rank's rows
+    const size_t cells = static_cast<size_t>(W) * static_cast<size_t>(rows);
+    double* d = w.hostbatch.ensure(std::max<size_t>(cells, 1));
+    if (rows) {
+        h2d(d, values, sizeof(double) * cells, w.st);
+        launch_transpose_in<T>(d, w.X[0].p + static_cast<size_t>(r0) * w.ld, static_cast<int>(rows), W, w.ld, w.st);
+    }
+    CK(cudaMemsetAsync(w.V.p, 0, sizeof(T) * static_cast<size_t>(n) * w.ld, w.st));
+    const size_t row_bytes = sizeof(T) * static_cast<size_t>(w.ld);
+    comm_allgather_rows(comm, w.X[0].p, row_bytes, range, w.st);
+
+    StepArgs<T> a{};
+    a.row_ptr = rp;
+    a.col = col;
+    a.deg = dg;
+    a.order = ord;
+    a.vel = w.V.p;
+    a.ld = w.ld;
+    a.n = static_cast<int>(rows);
+    a.W = W;
+    a.l = l;
+    a.members = members;
+    a.mu = static_cast<T>(mu);
+    a.alpha_uniform = static_cast<T>(alpha);
+    a.err = w.err.ensure(1);
+    CK(cudaMemsetAsync(a.err, 0xff, sizeof(unsigned long long), w.st));
+    uint32_t* F = nullptr;
+    uint32_t* bits = nullptr;
+    if (ee) {
+        F = w.flags.ensure(static_cast<size_t>(3) * members);
+        CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * 3 * members, w.st));
+        bits = w.orbits.ensure(static_cast<size_t>(3) * members);
+    }
+    int64_t it = 0;
+    for (; it < iters; ++it) {
+        a.x_in = w.X[it & 1].p;
+        a.x_out = w.X[(it + 1) & 1].p;
+        a.it = static_cast<int>(it);
+        if (ee) {
+            a.flags_prev = F + ((it + 2) % 3) * members;
+            a.flags_cur = F + (it % 3) * members;
+            a.flags_zero = F + ((it + 1) % 3) * members;
+        }
+        if (rows) launch_step<T>(a, ee, MODE_STEP, w.st);
+        else if (ee) CK(cudaMemsetAsync(a.flags_zero, 0, sizeof(uint32_t) * members, w.st));
+        if (ee && nr > 1) {  // the member's exit test sees every rank's rows
+            launch_bits_split(a.flags_cur, members, 3, bits, w.st);
+            comm_allreduce(comm, bits, static_cast<size_t>(3) * members, 4, true, w.st, "allreduce(exit bits)");
+            launch_bits_merge(bits, members, 3, a.flags_cur, w.st);
+        }
+        comm_allgather_rows(comm, a.x_out, row_bytes, range, w.st);
+        if (ee && ((it + 1) % 32 == 0) && it + 1 < iters) {  // the same decision on every rank
+            uint32_t* hf = w.host_flags(members);
+            d2h(hf, a.flags_cur, sizeof(uint32_t) * members, w.st);
+            CK(cudaStreamSynchronize(w.st));
+            bool any = false;
+            for (int m = 0; m < members && !any; ++m) any = ex_continue(hf[m]);
+            if (!any) {
+                ++it;
+                break;
+            }
+        }
+    }
+    comm_allreduce(comm, a.err, 1, 8, false, w.st, "allreduce(err)");
+    if (rows) {
+        launch_transpose_out<T>(w.X[it & 1].p + static_cast<size_t>(r0) * w.ld, d, static_cast<int>(rows), W, w.ld,
+                                w.st);
+        d2h(values, d, sizeof(double) * cells, w.st);
+    }
+    unsigned long long e = 0;
+    d2h(&e, a.err, sizeof(e), w.st);
+    CK(cudaStreamSynchronize(w.st));
+    CK(cudaGetLastError());
+    w.node_updates += it * static_cast<int64_t>(rows) * W;
+    if (e != ~0ull) {
+        const int64_t ei = static_cast<int64_t>(e & 0xffffffffull);
+        const int64_t em = static_cast<int64_t>(e >> 32);
+        if (err_it) *err_it = ei;
+        if (err_m) *err_m = em;
+        fail(LCB_NUMERIC, numeric_msg(ei, em));
+    }
+}
+
 template <class T>
 void laplacian_host(const DevGraph& g, const double* x, double* y, int64_t count) {
     const int W = static_cast<int>(count);
@@ -2243,6 +2456,22 @@ int lcb_ascend(const lcb_graph* g, double* values, int64_t n, int32_t l, int64_t
         else
             ascend_host<double>(g->g, values, n, l, B, alpha, iterations, momentum, early_exit != 0, trace,
                                 err_iter, err_member);
+    });
+}
+
+int lcb_ascend_rows(lcb_comm* comm, uint32_t n, int64_t row_begin, int64_t row_end, const int64_t* offsets,
+                    const uint32_t* adjacency, double* values, int32_t l, int64_t B, double alpha, int64_t iterations,
+                    double momentum, int32_t early_exit, int32_t precision, int device, int64_t* err_iter,
+                    int64_t* err_member) {
+    return guard([&] {
+        if (!offsets || (row_end > row_begin && !values)) fail(LCB_VALIDATION, "null argument");
+        if (comm_active(comm)) device = comm->device;
+        if (precision == LCB_FP32)
+            ascend_rows_host<float>(comm, n, row_begin, row_end, offsets, adjacency, values, l, B, alpha, iterations,
+                                    momentum, early_exit != 0, device, err_iter, err_member);
+        else
+            ascend_rows_host<double>(comm, n, row_begin, row_end, offsets, adjacency, values, l, B, alpha, iterations,
+                                     momentum, early_exit != 0, device, err_iter, err_member);
     });
 }
 

@@ -577,6 +577,31 @@ def ascend(g: Graph, state: DenseState, params: AscentParams, workers: int = 1,
                 trace(it, j, float(tr[it, j]))
 
 
+def ascend_rows(n: int, row_begin: int, row_end: int, offsets, adjacency, values, lift_dim: int, batch: int,
+                params: AscentParams, comm=None, precision: Optional[int] = None, device: Optional[int] = None):
+    """Row-sharded ascend (lcb_ascend_rows, north star 5): this rank holds the CSR rows
+    [row_begin, row_end) (offsets from 0, global column ids) and the slice
+    values [batch][lift_dim][rows] (float64, updated in place) of the DenseState; the
+    ranks of `comm` (dist.Comm) partition [0, n) in rank order.  Equals ``ascend`` on the
+    whole graph (fp64 bit for bit)."""
+    params.validate()
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    adj = np.ascontiguousarray(adjacency, dtype=np.uint32)
+    rows = row_end - row_begin
+    if off.shape != (rows + 1,):
+        raise ShapeError(f"ascend_rows: offsets must have {rows + 1} entries")
+    if values.dtype != np.float64 or not values.flags.c_contiguous or values.size != batch * lift_dim * rows:
+        raise ShapeError("ascend_rows: values must be a contiguous float64 [batch][lift_dim][rows] slice")
+    prec = default_precision() if precision is None else precision
+    dev = default_device() if device is None else device
+    ei, ej = C.c_int64(-1), C.c_int64(-1)
+    h = comm.handle if comm is not None else None
+    _check(_abi.lib().lcb_ascend_rows(h, int(n), int(row_begin), int(row_end), _ptr(off), _ptr(adj), _ptr(values),
+                                      int(lift_dim), int(batch), float(params.alpha), int(params.iterations),
+                                      float(params.momentum), int(bool(params.early_exit)), prec, int(dev),
+                                      C.byref(ei), C.byref(ej)))
+
+
 # ---------------------------------------------------------------------------
 # objectives (objectives.hpp)
 # ---------------------------------------------------------------------------

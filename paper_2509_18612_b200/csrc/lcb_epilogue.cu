@@ -5,9 +5,11 @@
 //
 // Reference lines: round_unlifted / round_lifted objectives.cpp:81-96,
 // cut_value :26-35, argmax solver.cpp:125-138, pm1_scaled :92-101.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "lcb_internal.h"
@@ -222,6 +224,107 @@ __global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_p
 }
 
 // ---------------------------------------------------------------------------
+// K4 as ONE kernel (north star 4): round + pack, grid barrier, bit-sliced cut counts,
+// then the last block to finish takes the first-max argmax of every segment and, when
+// no cross-rank reduction of the key is needed, extracts the winner's bits.  Launched
+// cooperatively (every block resident, so the grid barrier cannot deadlock); block b
+// counts the edges of assignment word b % words over its share of the rows.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64_t ld, int n, int members, int l,
+                                                  int lifted, uint32_t* __restrict__ Z, int words,
+                                                  const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                  unsigned long long* __restrict__ cuts,
+                                                  unsigned long long* __restrict__ done, int seg_size,
+                                                  int64_t member_base, unsigned long long* __restrict__ seg_keys,
+                                                  uint32_t* __restrict__ win_bits) {
+    namespace cg = cooperative_groups;
+    // ---- round + pack (objectives.cpp:81-96): one warp per (row, 32-member word)
+    {
+        const int lane = threadIdx.x & 31;
+        const int64_t total = static_cast<int64_t>(n) * words;
+        const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+        for (int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < total; t += stride) {
+            const int row = static_cast<int>(t / words);
+            const int w = static_cast<int>(t % words);
+            const int m = w * 32 + lane;
+            bool z = false;
+            if (m < members) {
+                const T* p = X + static_cast<int64_t>(row) * ld + static_cast<int64_t>(m) * l;
+                if (lifted) {
+                    double s = 0.0;
+                    for (int c = 0; c < l; ++c) s = __dadd_rn(s, static_cast<double>(p[c]));
+                    z = s >= 0.0;
+                } else {
+                    z = static_cast<double>(p[0]) > 0.0;
+                }
+            }
+            const uint32_t bits = __ballot_sync(0xffffffffu, z);
+            if (lane == 0) Z[static_cast<int64_t>(w) * n + row] = bits;
+        }
+    }
+    cg::this_grid().sync();
+    // ---- cut counts (objectives.cpp:26-35)
+    {
+        const int w = static_cast<int>(blockIdx.x % words);
+        const int parts = static_cast<int>(gridDim.x / words);
+        const int part = static_cast<int>(blockIdx.x / words);
+        const uint32_t* zw = Z + static_cast<int64_t>(w) * n;
+        uint32_t planes[16];
+        uint32_t cnt[32];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) planes[k] = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) cnt[b] = 0;
+        uint32_t adds = 0;
+        for (int r = part * blockDim.x + threadIdx.x; r < n; r += parts * blockDim.x) {
+            const uint32_t zu = __ldcg(zw + r);
+            const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
+            for (int k = beg; k < end; ++k) {
+                const int v = __ldg(col + k);
+                if (v > r) {
+                    planes_add(planes, zu ^ __ldcg(zw + v));
+                    if (++adds == 0xffffu) {
+                        planes_flush(planes, cnt);
+                        adds = 0;
+                    }
+                }
+            }
+        }
+        planes_flush(planes, cnt);
+        const int lane = threadIdx.x & 31;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t t = __reduce_add_sync(0xffffffffu, cnt[b]);
+            if (lane == b) mine = t;
+        }
+        if (mine) atomicAdd(cuts + w * 32 + lane, static_cast<unsigned long long>(mine));
+    }
+    // ---- the last block: argmax (solver.cpp:132-134), winner bits (solver.cpp:138)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1ull) == static_cast<unsigned long long>(gridDim.x) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    block_argmax(cuts, members, seg_size, member_base, seg_keys);
+    if (win_bits == nullptr) return;
+    const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(seg_keys);
+    const int64_t m = static_cast<int64_t>(0xffffffffull - (key & 0xffffffffull)) - member_base;
+    const int wsel = static_cast<int>(m >> 5), bsel = static_cast<int>(m & 31);
+    const int nwords = (n + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x >> 5; i < nwords; i += blockDim.x >> 5) {
+        const int v = i * 32 + lane;
+        const bool z = v < n && ((__ldcg(Z + static_cast<int64_t>(wsel) * n + v) >> bsel) & 1u);
+        const uint32_t word = __ballot_sync(0xffffffffu, z);
+        if (lane == 0) win_bits[i] = word;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // first-max argmax: key = cut << 32 | (0xffffffff - member) so that the max
 // key is the largest cut at the smallest member index (solver.cpp:132-134).
 // One block per segment (a batch; several when search candidates are batched).
@@ -361,6 +464,49 @@ void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned
     k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, cuts + words * 32, members,
                                                        seg_size, member_base, seg_keys);
 }
+
+template <typename T>
+void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int l, int lifted, uint32_t* Z,
+                     unsigned long long* cuts, int seg_size, int64_t member_base, unsigned long long* seg_keys,
+                     uint32_t* win_bits, cudaStream_t s) {
+    const int words = (members + 31) / 32;
+    cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * (static_cast<size_t>(words) * 32 + 1), s);
+    static std::atomic<int> per_sm[64];
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const int slot = dev >= 0 && dev < 64 ? dev : 0;
+    int occ = per_sm[slot].load(std::memory_order_relaxed);
+    if (!occ) {
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_epilogue<T>, 256, 0), "occupancy(k_epilogue)");
+        occ = std::max(1, occ);
+        per_sm[slot].store(occ, std::memory_order_relaxed);
+    }
+    // every block resident (grid barrier); a multiple of `words` blocks, <= one per 256 rows per word
+    const int resident = occ * num_sms(dev);
+    const int parts = std::max(1, std::min((g.n + 255) / 256, resident / words));
+    if (parts * words > resident)  // more words than resident blocks: the unfused kernels
+    {
+        launch_round_pack<T>(X, ld, g.n, members, l, lifted, Z, s);
+        launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
+        if (win_bits) launch_extract_winner(Z, g.n, seg_keys, member_base, members, win_bits, s, 0);
+        return;
+    }
+    unsigned long long* done = cuts + static_cast<size_t>(words) * 32;
+    int n = g.n, nw = words;
+    const int* rp = g.row_ptr;
+    const int* cl = g.col;
+    void* args[] = {&X, &ld, &n, &members, &l, &lifted, &Z, &nw, &rp, &cl, &cuts, &done, &seg_size,
+                    &member_base, &seg_keys, &win_bits};
+    count_launch();
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(parts * words),
+                                           dim3(256), args, 0, s),
+               "cudaLaunchCooperativeKernel(k_epilogue)");
+}
+template void launch_epilogue<float>(const DevGraph&, const float*, int64_t, int, int, int, uint32_t*,
+                                     unsigned long long*, int, int64_t, unsigned long long*, uint32_t*, cudaStream_t);
+template void launch_epilogue<double>(const DevGraph&, const double*, int64_t, int, int, int, uint32_t*,
+                                      unsigned long long*, int, int64_t, unsigned long long*, uint32_t*,
+                                      cudaStream_t);
 
 void launch_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
                    unsigned long long* seg_keys, cudaStream_t s) {

@@ -216,6 +216,12 @@ void launch_max_u32(const uint32_t* a, int64_t count, unsigned* out, cudaStream_
 void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts,
                       cudaStream_t s);
 // fused: cut counts + (last block) first-max argmax per segment; cuts needs words*32 + 1 entries
+// K4 in one cooperative kernel: round + pack -> grid barrier -> cut counts -> argmax of
+// every segment (seg_keys) -> winner bits of seg_keys[0] (win_bits, null: not extracted)
+template <typename T>
+void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int l, int lifted, uint32_t* Z,
+                     unsigned long long* cuts, int seg_size, int64_t member_base, unsigned long long* seg_keys,
+                     uint32_t* win_bits, cudaStream_t s);
 void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts, int members,
                        int seg_size, int64_t member_base, unsigned long long* seg_keys, cudaStream_t s);
 // segment argmax of packed keys; seg_keys[s] = max over members of segment s

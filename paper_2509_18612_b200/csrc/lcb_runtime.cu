@@ -1526,13 +1526,17 @@ struct Solver {
         mark = Clock::now();
         const int words = static_cast<int>((B + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * n);
-        launch_round_pack<T>(w.X[ir.final_buf].p, w.ld, n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
         unsigned long long* cuts = w.cuts.ensure(static_cast<size_t>(words) * 32 + 1);
         unsigned long long* key = w.keys.ensure(8);
-        launch_cut_argmax(g, Z, words, cuts, static_cast<int>(B), static_cast<int>(B), member_base, key, w.st);
-        comm_allreduce(comm, key, 1, 8, true, w.st, "allreduce(key)");
-        launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
-        comm_allreduce(comm, w.win.p, static_cast<size_t>(words_n), 4, true, w.st, "allreduce(winner)");
+        // K4, one kernel: round -> cut counts -> argmax -> (single rank) winner bits
+        const bool multi = comm_active(comm);
+        launch_epilogue<T>(g, w.X[ir.final_buf].p, w.ld, static_cast<int>(B), l, lifted ? 1 : 0, Z, cuts,
+                           static_cast<int>(B), member_base, key, multi ? nullptr : w.win.p, w.st);
+        if (multi) {
+            comm_allreduce(comm, key, 1, 8, true, w.st, "allreduce(key)");
+            launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);
+            comm_allreduce(comm, w.win.p, static_cast<size_t>(words_n), 4, true, w.st, "allreduce(winner)");
+        }
         d2h(w.h_keys, key, sizeof(unsigned long long), w.st);
         CK(cudaStreamSynchronize(w.st));
         CK(cudaGetLastError());
@@ -2573,12 +2577,11 @@ int lcb_round_cut_batch(const lcb_graph* g, const double* values, int32_t l, int
         launch_transpose_in<double>(d, w.X[0].p, G.n, W, w.ld, w.st);
         const int words = static_cast<int>((B + 31) / 32);
         uint32_t* Z = w.Z.ensure(static_cast<size_t>(words) * G.n);
-        launch_round_pack<double>(w.X[0].p, w.ld, G.n, static_cast<int>(B), l, lifted ? 1 : 0, Z, w.st);
         unsigned long long* c = w.cuts.ensure(static_cast<size_t>(words) * 32 + 1);
         unsigned long long* key = w.keys.ensure(8);
-        launch_cut_argmax(G, Z, words, c, static_cast<int>(B), static_cast<int>(B), 0, key, w.st);
         uint32_t* bits = w.win.ensure((G.n + 31) / 32);
-        launch_extract_winner(Z, G.n, key, 0, static_cast<int>(B), bits, w.st);
+        launch_epilogue<double>(G, w.X[0].p, w.ld, static_cast<int>(B), l, lifted ? 1 : 0, Z, c, static_cast<int>(B), 0,
+                                key, bits, w.st);
         std::vector<unsigned long long> hc(static_cast<size_t>(B));
         d2h(hc.data(), c, sizeof(unsigned long long) * B, w.st);
         d2h(w.h_keys, key, sizeof(unsigned long long), w.st);

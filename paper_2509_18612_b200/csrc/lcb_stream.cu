@@ -51,6 +51,9 @@ namespace {
 #endif
 constexpr int kR = LCB_STREAM_R;  // rows per tile = consumer warps per CTA
 constexpr int kThreadsS = 32 * (kR + 1);
+#ifndef LCB_STREAM_MINB
+#define LCB_STREAM_MINB 1  // resident CTAs per SM the register budget is sized for
+#endif
 #ifndef LCB_STREAM_STAGES
 #define LCB_STREAM_STAGES 4
 #endif
@@ -290,7 +293,7 @@ struct StreamSmem {
 };
 
 template <typename T, bool GEN, bool EE>
-__global__ void __launch_bounds__(kThreadsS, 1)
+__global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
     k_stream(StepArgs<T> a, int rowtiles, int slab0, int nslabs, const __grid_constant__ CUtensorMap mx,
              const __grid_constant__ CUtensorMap mv) {
     constexpr int E = Lanes<T>::E, H = Lanes<T>::H, SPAN = Lanes<T>::SPAN;

@@ -214,6 +214,14 @@ def measured_tensor_peak():
     return 1590.0, "fallback"
 
 
+def ncu_entry(config, precision, kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get(f"{config}_{precision}_{kernel}", {})
+
+
 def ncu_traffic(config, precision, kernel):
     """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed
     ncu capture of this workload (profiles/ncu_summary.json), if any."""
@@ -438,6 +446,7 @@ def roofline(kst, step_ms, name, precision):
                 "traffic": ncu_traffic(name, precision, kname), "kernel": kname,
                 "algorithmic_flops_per_launch": k_amount / max(k_launch, 1),
                 "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": twhich,
+                "tensor_pipe_active_pct": ncu_entry(name, precision, kname).get("tensor_pipe_active_pct"),
                 "model": "2*n^2*W algorithmic flops per iteration (SURVEY 8d). Executed MMA work differs per "
                          "32-node K step: bf16 hi/mid/lo planes before saturation, mid/lo skipped when all zero, "
                          "e4m3 MMAs on corner-valued steps (DESIGN.md K3)"}

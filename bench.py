@@ -262,6 +262,21 @@ def cpu_reference_step(rg, name, world, T, reps, threads):
     return ups, asc, sec, best
 
 
+def cpu_single_thread(rg):
+    """the reference's ascend on ONE host thread (the member-parallel reference
+    scales with threads up to B): a few members, T=2, timed around ref_ascend."""
+    import numpy as np
+
+    import oracle as O
+
+    B, T = 32, 2
+    x = np.random.default_rng(0).uniform(-1e-4, 1e-4, B * rg.n)
+    t0 = time.perf_counter()
+    O.ref_ascend(rg, x, 1, B, 0.05, T, 0.9, False, workers=1)
+    dt = time.perf_counter() - t0
+    return rg.n * B * T / dt, f"reference ascend, {B} members x T={T}, 1 thread ({dt:.1f} s)"
+
+
 def reference_graph(name):
     import oracle as O
 
@@ -514,6 +529,7 @@ def run_b200(args):
                                  f"instead of 500" + (f", {reps} solves" if reps > 1 else "") +
                                  f", {thr} host threads; node-updates / StageTimes.ascent_s ({asc:.1f} s of "
                                  f"{sec:.1f} s solve wall)"}
+                cpu["value_1_thread"], cpu["sample_1_thread"] = cpu_single_thread(rg)
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
         cfgd = config_dict(args.config, world, args.precision)

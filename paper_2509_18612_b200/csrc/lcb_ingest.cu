@@ -90,7 +90,7 @@ IngestResult ingest_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, in
     res.off.assign(static_cast<size_t>(n) + 1, 0);
     const unsigned grid = 148 * 8;
     if (m == 0) {
-        cuda_check(cudaMalloc(&res.col, sizeof(int) * 4), "cudaMalloc(col)");  // + K1s bulk-copy pad
+        res.col = static_cast<int*>(graph_alloc(sizeof(int) * 4));  // + K1s bulk-copy pad
         res.nnz = 0;
         return res;
     }
@@ -122,7 +122,7 @@ IngestResult ingest_edges_device(uint32_t n, const uint32_t* du, const uint32_t*
     res.off.assign(static_cast<size_t>(n) + 1, 0);
     const unsigned grid = 148 * 8;
     if (m == 0) {
-        cuda_check(cudaMalloc(&res.col, sizeof(int) * 4), "cudaMalloc(col)");  // + K1s bulk-copy pad
+        res.col = static_cast<int*>(graph_alloc(sizeof(int) * 4));  // + K1s bulk-copy pad
         res.nnz = 0;
         return res;
     }
@@ -154,7 +154,7 @@ IngestResult ingest_edges_device(uint32_t n, const uint32_t* du, const uint32_t*
     // CSR
     DevMem<int64_t> doff(static_cast<size_t>(n) + 1);
     int* col = nullptr;
-    cuda_check(cudaMalloc(&col, sizeof(int) * (static_cast<size_t>(nnz) + 4)), "cudaMalloc(col)");  // K1s copies 16-byte runs
+    col = static_cast<int*>(graph_alloc(sizeof(int) * (static_cast<size_t>(nnz) + 4)));  // K1s copies 16-byte runs
     count_launch();
     k_csr_from_sorted<<<grid, 256, 0, s>>>(d1.p, nnz, n, col, doff.p);
     cuda_check(cudaMemcpyAsync(res.off.data(), doff.p, sizeof(int64_t) * (static_cast<size_t>(n) + 1),
@@ -163,7 +163,7 @@ IngestResult ingest_edges_device(uint32_t n, const uint32_t* du, const uint32_t*
     count_d2h(sizeof(int64_t) * (static_cast<size_t>(n) + 1));
     const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
-        cudaFree(col);
+        graph_free(col);
         cuda_check(e, "sync(csr)");
     }
     res.col = col;

@@ -281,6 +281,10 @@ enum Opt : int {
 };
 int64_t option(Opt o);
 
+// graph arrays: the device's stream-ordered pool, cached (lcb_runtime.cu)
+void* graph_alloc(size_t bytes);
+void graph_free(void* p);
+
 // graph ingest from an edge list on the device (lcb_ingest.cu): adjacency `col` [nnz]
 // stays on the device (caller owns it), offsets come back to the host
 struct IngestResult {

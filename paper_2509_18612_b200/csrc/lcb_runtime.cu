@@ -197,20 +197,47 @@ struct HostStream {
 // ---------------------------------------------------------------------------
 // device graph
 // ---------------------------------------------------------------------------
+// Graph arrays come from the device's stream-ordered pool, kept cached (release threshold
+// at its maximum): a plain cudaFree of the ~40 MB of a config-4 graph took up to 200 ms
+// in the e2e loop (one graph per solve); pooled frees and re-allocations are immediate.
+void* graph_alloc(size_t bytes) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static bool pooled[64] = {};
+    if (dev >= 0 && dev < 64) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pooled[dev]) {
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t thr = ~0ull;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            pooled[dev] = true;
+        }
+    }
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, bytes ? bytes : 1, 0));
+    CK(cudaStreamSynchronize(0));  // usable from any stream
+    return p;
+}
+void graph_free(void* p) {
+    if (p) cudaFreeAsync(p, 0);
+}
+
 void free_graph(DevGraph& g) {
-    cudaFree(g.row_ptr);
-    cudaFree(g.col);
-    cudaFree(g.deg64);
-    cudaFree(g.deg32);
-    cudaFree(g.order);
-    cudaFree(g.res_info);
-    cudaFree(g.res_chunk);
-    cudaFree(g.res_heavy);
+    graph_free(g.row_ptr);
+    graph_free(g.col);
+    graph_free(g.deg64);
+    graph_free(g.deg32);
+    graph_free(g.order);
+    graph_free(g.res_info);
+    graph_free(g.res_chunk);
+    graph_free(g.res_heavy);
     g.res_heavy = nullptr;
-    cudaFree(g.dense_A);
+    graph_free(g.dense_A);
     g.dense_A = nullptr;
-    cudaFree(g.res_col);
-    cudaFree(g.res_col_fast);
+    graph_free(g.res_col);
+    graph_free(g.res_col_fast);
     g.res_info = nullptr;
     g.row_ptr = g.col = g.order = g.res_chunk = nullptr;
     g.res_col = g.res_col_fast = nullptr;
@@ -383,11 +410,11 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     }
 
     DeviceScope ds(device);
-    CK(cudaMalloc(&g.row_ptr, sizeof(int) * (n + 1)));
-    if (!dev_col) CK(cudaMalloc(&g.col, sizeof(int) * (nnz + 4)));  // K1s copies aligned 16-byte runs
-    CK(cudaMalloc(&g.deg64, sizeof(double) * n));
-    CK(cudaMalloc(&g.deg32, sizeof(float) * n));
-    CK(cudaMalloc(&g.order, sizeof(int) * n));
+    g.row_ptr = static_cast<decltype(g.row_ptr)>(graph_alloc(sizeof(int) * (n + 1)));
+    if (!dev_col) g.col = static_cast<decltype(g.col)>(graph_alloc(sizeof(int) * (nnz + 4)));  // K1s copies aligned 16-byte runs
+    g.deg64 = static_cast<decltype(g.deg64)>(graph_alloc(sizeof(double) * n));
+    g.deg32 = static_cast<decltype(g.deg32)>(graph_alloc(sizeof(float) * n));
+    g.order = static_cast<decltype(g.order)>(graph_alloc(sizeof(int) * n));
     h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
     // uint32 ids < n < 2^31: the same bits as int32, uploaded straight from the caller
     if (nnz && !dev_col) h2d(g.col, adj, sizeof(int) * nnz, 0);
@@ -414,7 +441,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         cudaMemGetInfo(&freeb, &totalb);
         const bool fits = dense_adjacency_bytes(static_cast<int>(n)) < freeb / 3;
         if (mode != 0 && fits && n >= 256 && (mode == 1 || (density >= 0.05 && n >= 4096))) {
-            CK(cudaMalloc(&g.dense_A, dense_adjacency_bytes(static_cast<int>(n))));
+            g.dense_A = static_cast<decltype(g.dense_A)>(graph_alloc(dense_adjacency_bytes(static_cast<int>(n))));
             build_dense_adjacency(g, g.dense_A, 0);
             CK(cudaDeviceSynchronize());
         }
@@ -523,10 +550,10 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             const int refine_passes = static_cast<int>(std::max<int64_t>(0, option(OPT_BANK_REFINE)));  // 0 disables
             if (!fast.empty() && refine_passes > 0 && bank_order == 2)
                 refine_bank_order(fast, rrp, static_cast<uint32_t>(H), n, refine_passes);
-            CK(cudaMalloc(&g.res_info, sizeof(uint32_t) * info.size()));
-            CK(cudaMalloc(&g.res_chunk, sizeof(int) * chunks));
-            CK(cudaMalloc(&g.res_heavy, sizeof(int) * hinfo.size()));
-            CK(cudaMalloc(&g.res_col, sizeof(uint16_t) * rcol.size()));
+            g.res_info = static_cast<decltype(g.res_info)>(graph_alloc(sizeof(uint32_t) * info.size()));
+            g.res_chunk = static_cast<decltype(g.res_chunk)>(graph_alloc(sizeof(int) * chunks));
+            g.res_heavy = static_cast<decltype(g.res_heavy)>(graph_alloc(sizeof(int) * hinfo.size()));
+            g.res_col = static_cast<decltype(g.res_col)>(graph_alloc(sizeof(uint16_t) * rcol.size()));
             h2d(g.res_info, info.data(), sizeof(uint32_t) * info.size(), 0);
             h2d(g.res_chunk, cbase.data(), sizeof(int) * chunks, 0);
             h2d(g.res_heavy, hinfo.data(), sizeof(int) * hinfo.size(), 0);
@@ -534,7 +561,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
             h2d(g.res_col, rcol.data(), sizeof(uint16_t) * rcol.size(), 0);
             g.res_len = static_cast<int64_t>(rcol.size());
             if (!fast.empty()) {
-                CK(cudaMalloc(&g.res_col_fast, sizeof(uint16_t) * fast.size()));
+                g.res_col_fast = static_cast<decltype(g.res_col_fast)>(graph_alloc(sizeof(uint16_t) * fast.size()));
                 h2d(g.res_col_fast, fast.data(), sizeof(uint16_t) * fast.size(), 0);
             }
         }
@@ -2370,7 +2397,7 @@ int lcb_graph_from_edges(uint32_t n, const uint32_t* eu, const uint32_t* ev, int
             r.col = nullptr;
             build_graph(h->g, n, r.off.data(), hadj.empty() ? nullptr : hadj.data(), device, col);
         } catch (...) {
-            if (r.col) cudaFree(r.col);
+            if (r.col) graph_free(r.col);
             free_graph(h->g);
             throw;
         }
@@ -2397,7 +2424,7 @@ int lcb_graph_parse(const char* text, int64_t len, int device, lcb_graph** out, 
             r.col = nullptr;
             build_graph(h->g, n, r.off.data(), hadj.empty() ? nullptr : hadj.data(), device, col);
         } catch (...) {
-            if (r.col) cudaFree(r.col);
+            if (r.col) graph_free(r.col);
             free_graph(h->g);
             throw;
         }

@@ -70,10 +70,17 @@ __device__ bool has_number(const char* t, int64_t p, int64_t end) {
     return p + 1 < end && t[p] == '.' && t[p + 1] >= '0' && t[p + 1] <= '9';
 }
 
-__global__ void k_line_flags(const char* __restrict__ t, int64_t len, uint8_t* __restrict__ flag) {
+__global__ void k_line_flags(const char* __restrict__ t, int64_t len, uint8_t* __restrict__ flag,
+                             unsigned long long* __restrict__ count) {
+    unsigned c = 0;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        flag[i] = (i == 0 || t[i - 1] == '\n') ? 1 : 0;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const bool f = i == 0 || t[i - 1] == '\n';
+        flag[i] = f ? 1 : 0;
+        c += f ? 1u : 0u;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
 }
 
 // one thread per line: kind, the two integers, weight present
@@ -155,14 +162,17 @@ IngestResult parse_edge_text(const char* text, int64_t len, uint32_t& n_out, boo
     count_h2d(static_cast<size_t>(len));
     // line starts
     Buf<uint8_t> flag(static_cast<size_t>(len));
-    count_launch();
-    k_line_flags<<<grid, 256, 0, s>>>(t.p, len, flag.p);
     Buf<int64_t> nsel(1);
+    int64_t lines = 0;
+    cuda_check(cudaMemsetAsync(nsel.p, 0, sizeof(int64_t), s), "memset(lines)");
+    count_launch();
+    k_line_flags<<<grid, 256, 0, s>>>(t.p, len, flag.p, reinterpret_cast<unsigned long long*>(nsel.p));
+    cuda_check(cudaMemcpyAsync(&lines, nsel.p, sizeof(lines), cudaMemcpyDeviceToHost, s), "d2h(line count)");
+    cuda_check(cudaStreamSynchronize(s), "sync(line count)");
     size_t tb = 0;
     cub::DeviceSelect::Flagged(nullptr, tb, cub::CountingInputIterator<int64_t>(0), flag.p,
                                static_cast<int64_t*>(nullptr), nsel.p, len, s);
-    int64_t lines = 0;
-    Buf<int64_t> start(static_cast<size_t>(len));
+    Buf<int64_t> start(static_cast<size_t>(lines));  // exactly the line starts
     {
         Buf<uint8_t> tmp(tb);
         cuda_check(cub::DeviceSelect::Flagged(tmp.p, tb, cub::CountingInputIterator<int64_t>(0), flag.p, start.p,

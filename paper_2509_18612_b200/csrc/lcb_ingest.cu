@@ -70,8 +70,8 @@ __global__ void k_csr_from_sorted(const uint64_t* __restrict__ d, int64_t nnz, u
 template <class T>
 struct DevMem {
     T* p = nullptr;
-    explicit DevMem(size_t count) { cuda_check(cudaMalloc(&p, sizeof(T) * (count ? count : 1)), "cudaMalloc(ingest)"); }
-    ~DevMem() { cudaFree(p); }
+    explicit DevMem(size_t count) { p = static_cast<T*>(pool_alloc(sizeof(T) * (count ? count : 1), 0)); }
+    ~DevMem() { pool_free(p, 0); }
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
 };

@@ -284,6 +284,9 @@ int64_t option(Opt o);
 // graph arrays: the device's stream-ordered pool, cached (lcb_runtime.cu)
 void* graph_alloc(size_t bytes);
 void graph_free(void* p);
+// stream-ordered temporaries from the same cached pool (ingest / parse scratch)
+void* pool_alloc(size_t bytes, cudaStream_t st);
+void pool_free(void* p, cudaStream_t st);
 
 // graph ingest from an edge list on the device (lcb_ingest.cu): adjacency `col` [nnz]
 // stays on the device (caller owns it), offsets come back to the host

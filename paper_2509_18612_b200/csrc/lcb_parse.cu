@@ -145,8 +145,8 @@ __global__ void k_check_edges(const uint8_t* __restrict__ kind, const long long*
 template <class T>
 struct Buf {
     T* p = nullptr;
-    explicit Buf(size_t count) { cuda_check(cudaMalloc(&p, sizeof(T) * (count ? count : 1)), "cudaMalloc(parse)"); }
-    ~Buf() { cudaFree(p); }
+    explicit Buf(size_t count) { p = static_cast<T*>(pool_alloc(sizeof(T) * (count ? count : 1), 0)); }
+    ~Buf() { pool_free(p, 0); }
     Buf(const Buf&) = delete;
     Buf& operator=(const Buf&) = delete;
 };

@@ -200,7 +200,7 @@ struct HostStream {
 // Graph arrays come from the device's stream-ordered pool, kept cached (release threshold
 // at its maximum): a plain cudaFree of the ~40 MB of a config-4 graph took up to 200 ms
 // in the e2e loop (one graph per solve); pooled frees and re-allocations are immediate.
-void* graph_alloc(size_t bytes) {
+void* pool_alloc(size_t bytes, cudaStream_t st) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     static std::mutex mu;
@@ -216,13 +216,18 @@ void* graph_alloc(size_t bytes) {
         }
     }
     void* p = nullptr;
-    CK(cudaMallocAsync(&p, bytes ? bytes : 1, 0));
+    CK(cudaMallocAsync(&p, bytes ? bytes : 1, st));
+    return p;
+}
+void pool_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+void* graph_alloc(size_t bytes) {
+    void* p = pool_alloc(bytes, 0);
     CK(cudaStreamSynchronize(0));  // usable from any stream
     return p;
 }
-void graph_free(void* p) {
-    if (p) cudaFreeAsync(p, 0);
-}
+void graph_free(void* p) { pool_free(p, 0); }
 
 void free_graph(DevGraph& g) {
     graph_free(g.row_ptr);

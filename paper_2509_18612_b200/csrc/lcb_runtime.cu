@@ -1147,11 +1147,12 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         return static_cast<int64_t>(v > 0 ? v : (126 << 20));
     }();
     const int64_t so = option(OPT_SLAB_OUTER);
-    const bool slab_outer = (!ee || sspan % l == 0) && nslabs > 1 &&
+    // (a trace needs every column after every iteration: iteration-major then)
+    const bool slab_outer = (!ee || sspan % l == 0) && nslabs > 1 && !trace_host &&
                             (so == 1 || (so < 0 && static_cast<int64_t>(g.n) * 32 * nslabs * 2 > l2b / 2));
     // default 1: K1s for every streaming step (config 4: 1.83 vs 3.6 ms/iteration, config 5:
     // 148 vs 166 us); -1: K1s only where the slab-major order is needed
-    const bool use_stream = (stream_mode == 1 || (stream_mode < 0 && slab_outer)) && !trace_host &&
+    const bool use_stream = (stream_mode == 1 || (stream_mode < 0 && slab_outer)) &&
                             w.ld % sspan == 0 &&
                             static_cast<int64_t>(g.n) * 36 * (slab_outer ? 1 : nslabs) < (int64_t(1) << 32);
     static const int64_t l2_bytes = [] {
@@ -1185,7 +1186,7 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
         // only, X is completed by launch_xcode_fill after a slab's (or the run's) last
         // iteration.  Not with per-segment stop iterations: a stopped segment's X must stay
         // complete while later iterations overwrite the codes.
-        a.xskip = (option(OPT_XCODE) != 0 && !seg_iters) ? 1 : 0;
+        a.xskip = (option(OPT_XCODE) != 0 && !seg_iters && !trace_host) ? 1 : 0;  // a trace reads X
     }
     if (use_stream && slab_outer) {
         // ---- K1s, slab-outer: for each 512-byte column slab, all its iterations

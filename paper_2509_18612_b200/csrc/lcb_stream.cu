@@ -258,6 +258,11 @@ constexpr int kClaim = LCB_STREAM_CLAIM;  // tiles per dynamic claim
 // always load their own stored x (the SMEM goes to deeper v staging)
 constexpr bool kXBox = LCB_STREAM_XBOX != 0;
 
+__device__ __forceinline__ uint32_t sign_bit(float v) { return __float_as_uint(v) >> 31; }
+__device__ __forceinline__ uint32_t sign_bit(double v) {
+    return static_cast<uint32_t>(static_cast<unsigned long long>(__double_as_longlong(v)) >> 63);
+}
+
 // every one of the E values finite: the products with zero are +-0 exactly then, NaN otherwise
 __device__ __forceinline__ bool finite_all(const float* r) {
     float z0 = 0.f, z1 = 0.f;
@@ -508,6 +513,10 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                 cp_async16(dc, cin + line * 32u);
                 cp_async16(dc + 16u, cin + line * 32u + 16u);
                 cp_async4(a_flags + static_cast<uint32_t>(buf) * 128u, fin + line);
+            } else if (k0 == 0 && k < deg + 2 && deg <= 30) {  // zero lines up to a multiple of 3 (fast path)
+                const uint32_t dc = a_codes + static_cast<uint32_t>(buf) * 1024u;
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dc), "r"(0u) : "memory");
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dc + 16u), "r"(0u) : "memory");
             }
             if (k0 == 0 && lane >= 24 && a.xskip && sm.xfl[st][j] == 0) {  // own line, 4 bytes per lane
                 const uint32_t line = static_cast<uint32_t>(sl) * n32 + static_cast<uint32_t>(row);
@@ -582,8 +591,11 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                 const uint8_t* cb = &sm.codes[j][buf][0][lane];
                 auto spread = [](uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; };
                 uint32_t q0 = 0, q1 = 0;  // +1 counts: byte e of q0 = element e, of q1 = element 4 + e
+                // the staged lines past the degree are zero (stage_codes pads up to a multiple of
+                // 3 when that fits the 32 slots): zero signs count no +1
+                const int kfull = deg <= 30 ? deg : deg - deg % 3;
                 int k = 0;
-                for (; k + 3 <= deg; k += 3) {
+                for (; k < kfull; k += 3) {
                     const uint32_t b0 = cb[32 * k], b1 = cb[32 * (k + 1)], b2 = cb[32 * (k + 2)];
                     const uint32_t par = b0 ^ b1 ^ b2;
                     const uint32_t maj = (b0 & b1) | (b2 & (b0 | b1));
@@ -595,10 +607,26 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                     q0 += spread(b & 0xFu);
                     if constexpr (E == 8) q1 += spread(b >> 4);
                 }
+                if constexpr (sizeof(T) == 4) {
+                    // fp32: the doubled count byte (2c <= 64) as the low mantissa byte of 2^22
+                    // (0x4A8000xx = 2^22 + c, exact), then deg - 2c = fma(-2, 2^22 + c, deg + 2^23)
+                    // exactly (deg + 2^23 is representable, the fma rounds once an exact
+                    // integer).  Only a zero sum differs from the sequential -(+0.0) (+0.0
+                    // here), and only for isolated rows, where y = 0 * x + (+-0) leaves v = +0
+                    // and x unchanged either way.
+                    const float dbias = static_cast<float>(deg) + 8388608.f;
+                    const uint32_t d0 = q0 << 1, d1 = q1 << 1;
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const uint32_t c = __byte_perm(e < 4 ? q0 : q1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
-                    nacc[e] = -static_cast<T>(2 * static_cast<int>(c) - deg);
+                    for (int e = 0; e < E; ++e) {
+                        const uint32_t cf = __byte_perm(e < 4 ? d0 : d1, 0x4A800000u, 0x7640u + static_cast<uint32_t>(e & 3));
+                        nacc[e] = __fmaf_rn(-2.f, __uint_as_float(cf), dbias);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const uint32_t c = __byte_perm(e < 4 ? q0 : q1, 0u, 0x4440u + static_cast<uint32_t>(e & 3));
+                        nacc[e] = -static_cast<T>(2 * static_cast<int>(c) - deg);
+                    }
                 }
             } else {
                 int cur = buf;  // buffer holding the current 32-neighbour chunk
@@ -754,8 +782,14 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                         if (xo[e] != T(1) && xo[e] != T(-1)) b |= EX_NOTB;
                         ebits |= b << (3 * e);
                     }
-                    sign |= (xo[e] > T(0) ? 1u : 0u) << e;
                     interior |= fabs(xo[e]) != T(1);
+                }
+                if (!interior) {  // all +-1: the sign bit alone decides x > 0
+#pragma unroll
+                    for (int e = 0; e < E; ++e) sign |= (sign_bit(xo[e]) ^ 1u) << e;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) sign |= (xo[e] > T(0) ? 1u : 0u) << e;
                 }
             } else {
                 T vn[E];

@@ -919,12 +919,16 @@ struct PooledWork {
 // fp32 takes K2 whenever the slab fits, at any batch width: K2 sums each row in its own
 // (bank-balanced) neighbour order, so choosing the kernel by W would make a member's fp32
 // trajectory depend on the batch width and the rank count (test_ascent.cpp:110-136).
+// fp64 has no such constraint (every kernel is bit-exact): K2 holds one fp64 column per CTA
+// and stays near 7e10 node-updates/s at any width, while K1s grows with the batch, so fp64
+// streams once n * W >= 2e6 (measured on BA n = 2k / 5k / 10k, W = 256 .. 2048: config 2 at
+// W = 1024 137 -> 64 us per iteration; profiles/round2_k1s.md).
 bool resident_preferred(const DevGraph& g, int W, size_t elem) {
-    (void)g;
-    (void)W;
-    (void)elem;
     const int64_t mode = option(OPT_RESIDENT);  // -1 auto, 0 never, 1 always (when it fits)
-    return mode != 0;
+    if (mode == 1) return true;
+    if (mode == 0) return false;
+    if (elem == 8 && static_cast<int64_t>(g.n) * W >= 2000000) return false;
+    return true;
 }
 
 struct IterResult {

@@ -245,6 +245,10 @@ __device__ __forceinline__ void pga_raw_neg2(const double* x, const double* nax,
 #define LCB_STREAM_CLAIM 1
 #endif
 constexpr int kClaim = LCB_STREAM_CLAIM;  // tiles per dynamic claim
+#ifndef LCB_STREAM_ILV
+#define LCB_STREAM_ILV 1
+#endif
+constexpr bool kInterleave = LCB_STREAM_ILV != 0;  // tile order: slab-interleaved (1) or slab-major (0)
 #ifndef LCB_STREAM_STATIC
 #define LCB_STREAM_STATIC 0
 #endif
@@ -338,6 +342,10 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
         // the last tile a sentinel stage (slab = -1) tells the consumers to stop.
         const uint64_t pol = policy_evict_first();
         constexpr int P = kLook;
+        // tile t -> (slab, first row): slab-interleaved, so the hub rows at the front of every
+        // slab (BA graphs) are claimed first and the CTAs holding them catch up on the rest
+        auto tile_slab = [&](int t) { return kInterleave ? t % nslabs : t / rowtiles; };
+        auto tile_row0 = [&](int t) { return (kInterleave ? t / nslabs : t - (t / rowtiles) * rowtiles) * kR; };
         // per claim: lane j <= R: row_ptr[min(r0 + j, n)]; the tile index; lane j < R: the
         // flag of row r0 + j's slab in the input codes (x-code mode; 0 = x is in the code)
         int qrp[P], qt[P], qfl[P];
@@ -367,8 +375,8 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
             int rp = 0;
             fl = 1;
             if (t < ntiles && lane <= kR) {
-                int sl = t / rowtiles;
-                const int row = (t - sl * rowtiles) * kR + lane;
+                int sl = tile_slab(t);
+                const int row = tile_row0(t) + lane;
                 rp = __ldg(a.row_ptr + min(row, a.n));
                 if (pfin && lane < kR) {
                     if (a.it & 1) sl = nslabs - 1 - sl;
@@ -402,8 +410,8 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                 qrp[q] = claim(qt[q], qfl[q]);
                 const int end = __shfl_down_sync(0xffffffffu, beg, 1);
                 const int first = __shfl_sync(0xffffffffu, beg, 0), last = __shfl_sync(0xffffffffu, beg, kR);
-                int sl = t / rowtiles;
-                const int r0 = (t - sl * rowtiles) * kR;
+                int sl = tile_slab(t);
+                const int r0 = tile_row0(t);
                 if (a.it & 1) sl = nslabs - 1 - sl;  // snake: reuse the slab just written
                 const int abeg = first & ~3;
                 const int ncopy = min(((last + 3) & ~3) - abeg, kColBuf);  // staged prefix of the tile's run

@@ -456,6 +456,7 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
     auto member_of = [&](int slab, int e) { return (a.col_base + col_of(slab, e)) / a.l; };
     int cur_slab = -1;
     uint32_t act_bits = 0;  // which elements step at this iteration (bit e)
+    uint32_t valid_bits = 0;  // which elements are batch columns (not padding past W)
     bool all_act = false;
     uint32_t ebits = 0;     // 3 exit bits per element (EE)
     auto flush_bits = [&]() {
@@ -476,9 +477,11 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
         if (cur_slab >= 0) flush_bits();
         cur_slab = slab;
         act_bits = 0;
+        valid_bits = 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             bool act = col_of(slab, e) < a.W;
+            valid_bits |= act ? 1u << e : 0u;
             if constexpr (GEN) {
                 if (act) {
                     const int m = member_of(slab, e);
@@ -823,7 +826,9 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                     xo[e] = act ? cl : xv[e];
                     vv[e] = act ? vn[e] : vv[e];
                     sign |= (xo[e] > T(0) ? 1u : 0u) << e;
-                    interior |= fabs(xo[e]) != T(1);
+                    // padding columns past the batch never reach the corners (they stay 0) and
+                    // are never read for a real member: they do not keep the slab interior
+                    interior |= ((valid_bits >> e) & 1u) && fabs(xo[e]) != T(1);
                 }
             }
             if (bad) {

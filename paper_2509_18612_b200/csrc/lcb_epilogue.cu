@@ -14,6 +14,10 @@
 
 #include "lcb_internal.h"
 
+#ifndef LCB_EPI_UNROLL
+#define LCB_EPI_UNROLL 4
+#endif
+
 namespace lcb {
 
 namespace {
@@ -140,6 +144,45 @@ __device__ __forceinline__ void planes_flush(uint32_t (&p)[16], uint32_t (&cnt)[
     for (int k = 0; k < 16; ++k) p[k] = 0;
 }
 
+// Accumulate the cut edges (u < v) of rows [first, n) with the given stride into the
+// thread's bit planes.  Sparse graphs: one row per thread.  Dense graphs (average degree
+// above 64): one row per warp, the lanes striding over its neighbours, so a 10k-neighbour
+// row is not one thread's dependent load chain.
+template <bool COHERENT>
+__device__ __forceinline__ void cut_rows(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                         const uint32_t* __restrict__ zw, int n, int part, int parts, bool warp_rows,
+                                         uint32_t (&planes)[16], uint32_t (&cnt)[32]) {
+    auto zload = [&](int i) { return COHERENT ? __ldcg(zw + i) : __ldg(zw + i); };
+    uint32_t adds = 0;
+    auto add = [&](uint32_t d) {
+        planes_add(planes, d);
+        if (++adds == 0xffffu) {
+            planes_flush(planes, cnt);
+            adds = 0;
+        }
+    };
+    if (!warp_rows) {
+        for (int r = part * blockDim.x + threadIdx.x; r < n; r += parts * blockDim.x) {
+            const uint32_t zu = zload(r);
+            const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
+            for (int k = beg; k < end; ++k) {
+                const int v = __ldg(col + k);
+                if (v > r) add(zu ^ zload(v));  // each undirected edge once (objectives.cpp:33)
+            }
+        }
+    } else {
+        const int wpb = blockDim.x >> 5, lane = threadIdx.x & 31;
+        for (int r = part * wpb + (threadIdx.x >> 5); r < n; r += parts * wpb) {
+            const uint32_t zu = zload(r);
+            const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
+            for (int k = beg + lane; k < end; k += 32) {
+                const int v = __ldg(col + k);
+                if (v > r) add(zu ^ zload(v));
+            }
+        }
+    }
+}
+
 // first-max argmax over `members` cuts in segments of seg_size, by one block
 __device__ void block_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
                              unsigned long long* seg_keys) {
@@ -178,7 +221,8 @@ __global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_p
                                                    const uint32_t* __restrict__ Z, int n,
                                                    unsigned long long* __restrict__ cuts,
                                                    unsigned long long* __restrict__ done, int members, int seg_size,
-                                                   int64_t member_base, unsigned long long* __restrict__ seg_keys) {
+                                                   int64_t member_base, unsigned long long* __restrict__ seg_keys,
+                                                   int warp_rows) {
     const int w = blockIdx.y;
     const uint32_t* zw = Z + static_cast<int64_t>(w) * n;
     uint32_t planes[16];
@@ -187,21 +231,7 @@ __global__ void __launch_bounds__(256) k_cut_count(const int* __restrict__ row_p
     for (int k = 0; k < 16; ++k) planes[k] = 0;
 #pragma unroll
     for (int b = 0; b < 32; ++b) cnt[b] = 0;
-    uint32_t adds = 0;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-        const uint32_t zu = __ldg(zw + r);
-        const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
-        for (int k = beg; k < end; ++k) {
-            const int v = __ldg(col + k);
-            if (v > r) {  // each undirected edge once (objectives.cpp:33)
-                planes_add(planes, zu ^ __ldg(zw + v));
-                if (++adds == 0xffffu) {
-                    planes_flush(planes, cnt);
-                    adds = 0;
-                }
-            }
-        }
-    }
+    cut_rows<false>(row_ptr, col, zw, n, blockIdx.x, gridDim.x, warp_rows != 0, planes, cnt);
     planes_flush(planes, cnt);
     const int lane = threadIdx.x & 31;
     uint32_t mine = 0;
@@ -237,7 +267,8 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
                                                   unsigned long long* __restrict__ cuts,
                                                   unsigned long long* __restrict__ done, int seg_size,
                                                   int64_t member_base, unsigned long long* __restrict__ seg_keys,
-                                                  uint32_t* __restrict__ win_bits) {
+                                                  uint32_t* __restrict__ win_bits, int warp_rows,
+                                                  uint32_t* __restrict__ Zt) {
     namespace cg = cooperative_groups;
     // ---- round + pack (objectives.cpp:81-96): one warp per (row, 32-member word)
     {
@@ -260,12 +291,62 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
                 }
             }
             const uint32_t bits = __ballot_sync(0xffffffffu, z);
-            if (lane == 0) Z[static_cast<int64_t>(w) * n + row] = bits;
+            if (lane == 0) {
+                Z[static_cast<int64_t>(w) * n + row] = bits;
+                if (Zt) Zt[static_cast<int64_t>(row) * 8 + w] = bits;
+            }
         }
     }
     cg::this_grid().sync();
     // ---- cut counts (objectives.cpp:26-35)
-    {
+    if (Zt) {
+        // dense graphs, <= 8 words: warp j of every block counts word j over the block's rows;
+        // the 8 warps read the same column runs and the same 32-byte node-major Zt lines, so
+        // those loads hit L1 after the first warp
+        const int j = static_cast<int>(threadIdx.x >> 5);
+        if (j < words) {
+            const int lane = threadIdx.x & 31;
+            uint32_t planes[16];
+            uint32_t cnt[32];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) planes[k] = 0;
+#pragma unroll
+            for (int b = 0; b < 32; ++b) cnt[b] = 0;
+            uint32_t adds = 0;
+            for (int r = blockIdx.x; r < n; r += gridDim.x) {
+                const uint32_t zu = Zt[static_cast<int64_t>(r) * 8 + j];
+                const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
+                // kU neighbours per lane in flight (the column and Zt loads are independent)
+                constexpr int kU = LCB_EPI_UNROLL;
+                for (int k = beg + lane; k < end; k += 32 * kU) {
+                    int v[kU];
+                    uint32_t zv[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) v[u] = k + 32 * u < end ? __ldg(col + k + 32 * u) : -1;
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) zv[u] = v[u] > r ? Zt[static_cast<int64_t>(v[u]) * 8 + j] : zu;
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        if (v[u] > r) {  // each undirected edge once (objectives.cpp:33)
+                            planes_add(planes, zu ^ zv[u]);
+                            if (++adds == 0xffffu) {
+                                planes_flush(planes, cnt);
+                                adds = 0;
+                            }
+                        }
+                    }
+                }
+            }
+            planes_flush(planes, cnt);
+            uint32_t mine = 0;
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+                const uint32_t t = __reduce_add_sync(0xffffffffu, cnt[b]);
+                if (lane == b) mine = t;
+            }
+            if (mine) atomicAdd(cuts + j * 32 + lane, static_cast<unsigned long long>(mine));
+        }
+    } else {
         const int w = static_cast<int>(blockIdx.x % words);
         const int parts = static_cast<int>(gridDim.x / words);
         const int part = static_cast<int>(blockIdx.x / words);
@@ -276,21 +357,7 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
         for (int k = 0; k < 16; ++k) planes[k] = 0;
 #pragma unroll
         for (int b = 0; b < 32; ++b) cnt[b] = 0;
-        uint32_t adds = 0;
-        for (int r = part * blockDim.x + threadIdx.x; r < n; r += parts * blockDim.x) {
-            const uint32_t zu = __ldcg(zw + r);
-            const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
-            for (int k = beg; k < end; ++k) {
-                const int v = __ldg(col + k);
-                if (v > r) {
-                    planes_add(planes, zu ^ __ldcg(zw + v));
-                    if (++adds == 0xffffu) {
-                        planes_flush(planes, cnt);
-                        adds = 0;
-                    }
-                }
-            }
-        }
+        cut_rows<true>(row_ptr, col, zw, n, part, parts, warp_rows != 0, planes, cnt);
         planes_flush(planes, cnt);
         const int lane = threadIdx.x & 31;
         uint32_t mine = 0;
@@ -452,7 +519,8 @@ void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned 
     cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * static_cast<size_t>(words) * 32, s);
     const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
     count_launch();
-    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, nullptr, 0, 1, 0, nullptr);
+    k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, nullptr, 0, 1, 0, nullptr,
+                                                       g.deg_mean > 64.0 ? 1 : 0);
 }
 
 void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts, int members,
@@ -462,7 +530,7 @@ void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned
     const int per_word = std::max(1, std::min((g.n + 255) / 256, (8 * num_sms(g.device)) / words + 1));
     count_launch();
     k_cut_count<<<dim3(per_word, words), 256, 0, s>>>(g.row_ptr, g.col, Z, g.n, cuts, cuts + words * 32, members,
-                                                       seg_size, member_base, seg_keys);
+                                                       seg_size, member_base, seg_keys, g.deg_mean > 64.0 ? 1 : 0);
 }
 
 template <typename T>
@@ -483,8 +551,16 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     }
     // every block resident (grid barrier); a multiple of `words` blocks, <= one per 256 rows per word
     const int resident = occ * num_sms(dev);
-    const int parts = std::max(1, std::min((g.n + 255) / 256, resident / words));
-    if (parts * words > resident)  // more words than resident blocks: the unfused kernels
+    // dense graphs with <= 8 words: every block counts all words (warp j = word j) over its
+    // rows, sharing the column and Zt loads in L1; Zt = node-major copy of Z [n][8]
+    const bool dense_block = g.deg_mean > 64.0 && words <= 8;
+    int parts = std::max(1, std::min((g.n + 255) / 256, resident / words));
+    int grid = parts * words;
+    uint32_t* Zt = nullptr;
+    if (dense_block) {
+        grid = std::max(1, std::min(g.n, resident));
+        Zt = static_cast<uint32_t*>(pool_alloc(sizeof(uint32_t) * 8 * static_cast<size_t>(g.n), s));
+    } else if (parts * words > resident)  // more words than resident blocks: the unfused kernels
     {
         launch_round_pack<T>(X, ld, g.n, members, l, lifted, Z, s);
         launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
@@ -495,12 +571,14 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     int n = g.n, nw = words;
     const int* rp = g.row_ptr;
     const int* cl = g.col;
+    int warp_rows = g.deg_mean > 64.0 ? 1 : 0;
     void* args[] = {&X, &ld, &n, &members, &l, &lifted, &Z, &nw, &rp, &cl, &cuts, &done, &seg_size,
-                    &member_base, &seg_keys, &win_bits};
+                    &member_base, &seg_keys, &win_bits, &warp_rows, &Zt};
     count_launch();
-    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(parts * words),
-                                           dim3(256), args, 0, s),
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(grid), dim3(256), args,
+                                           0, s),
                "cudaLaunchCooperativeKernel(k_epilogue)");
+    if (Zt) pool_free(Zt, s);
 }
 template void launch_epilogue<float>(const DevGraph&, const float*, int64_t, int, int, int, uint32_t*,
                                      unsigned long long*, int, int64_t, unsigned long long*, uint32_t*, cudaStream_t);

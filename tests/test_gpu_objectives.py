@@ -34,3 +34,23 @@ def test_round_lifted_inclusive_and_column_order(l):
     for j in range(B):
         want = O.round_lifted(s.member(j), n, l)
         assert np.array_equal(lc.round_lifted(s, j), want), j
+
+
+@pytest.mark.parametrize("p", [0.02, 0.5])
+def test_cut_counts_dense_warp_rows_vs_oracle(p):
+    """Cut counting on a dense graph (average degree > 64: one row per warp, lanes striding
+    over the neighbours) and a sparse one (one row per thread): every count equals the
+    oracle's, through lcb_cut_values and through the fused epilogue (round_cut_batch)."""
+    cg = O.generate_er(700, p, 3)
+    g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+    rng = np.random.default_rng(int(p * 100))
+    Z = rng.integers(0, 2, (70, cg.n), dtype=np.uint8)
+    got = lc.cut_values(g, Z)
+    want = [O.cut_value(cg, z) for z in Z]
+    assert got.tolist() == want
+    B = 70
+    s = lc.DenseState(cg.n, 1, B)
+    s.values[:] = rng.normal(0, 1, B * cg.n)
+    cuts, _, _, _ = lc.round_cut_batch(g, s, lifted=False)
+    zz = (s.values.reshape(B, cg.n) > 0).astype(np.uint8)
+    assert cuts.tolist() == [O.cut_value(cg, row) for row in zz]

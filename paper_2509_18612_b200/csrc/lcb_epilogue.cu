@@ -575,10 +575,19 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     void* args[] = {&X, &ld, &n, &members, &l, &lifted, &Z, &nw, &rp, &cl, &cuts, &done, &seg_size,
                     &member_base, &seg_keys, &win_bits, &warp_rows, &Zt};
     count_launch();
-    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(grid), dim3(256), args,
-                                           0, s),
-               "cudaLaunchCooperativeKernel(k_epilogue)");
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(grid),
+                                                      dim3(256), args, 0, s);
     if (Zt) pool_free(Zt, s);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        // other work holds part of the device (the grid barrier needs every block resident):
+        // the same epilogue as separate launches
+        (void)cudaGetLastError();
+        launch_round_pack<T>(X, ld, g.n, members, l, lifted, Z, s);
+        launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
+        if (win_bits) launch_extract_winner(Z, g.n, seg_keys, member_base, members, win_bits, s, 0);
+        return;
+    }
+    cuda_check(e, "cudaLaunchCooperativeKernel(k_epilogue)");
 }
 template void launch_epilogue<float>(const DevGraph&, const float*, int64_t, int, int, int, uint32_t*,
                                      unsigned long long*, int, int64_t, unsigned long long*, uint32_t*, cudaStream_t);

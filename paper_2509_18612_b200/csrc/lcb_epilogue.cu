@@ -165,9 +165,21 @@ __device__ __forceinline__ void cut_rows(const int* __restrict__ row_ptr, const 
         for (int r = part * blockDim.x + threadIdx.x; r < n; r += parts * blockDim.x) {
             const uint32_t zu = zload(r);
             const int beg = __ldg(row_ptr + r), end = __ldg(row_ptr + r + 1);
-            for (int k = beg; k < end; ++k) {
+            int k = beg;
+            for (; k + 4 <= end; k += 4) {  // four independent column / Z loads in flight
+                int v[4];
+                uint32_t zv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(col + k + u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) zv[u] = v[u] > r ? zload(v[u]) : zu;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (v[u] > r) add(zu ^ zv[u]);  // each undirected edge once (objectives.cpp:33)
+            }
+            for (; k < end; ++k) {
                 const int v = __ldg(col + k);
-                if (v > r) add(zu ^ zload(v));  // each undirected edge once (objectives.cpp:33)
+                if (v > r) add(zu ^ zload(v));
             }
         }
     } else {

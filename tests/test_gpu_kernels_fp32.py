@@ -133,14 +133,19 @@ def test_fp32_member_independent_of_batch_width(c2):
     assert np.array_equal(wide[:136 * n], narrow)
 
 
-def test_k1_and_k1s_bitwise_equal_fp32(c2):
+@pytest.mark.parametrize("ee,l,B", [(False, 1, 384), (True, 1, 384), (True, 2, 150)])
+def test_k1_and_k1s_bitwise_equal_fp32(c2, ee, l, B):
+    """K1 (saturation codes on / off) and K1s (x-code mode, slab-major and iteration-major)
+    give the same fp32 iterate bit for bit, with and without early exit, unlifted and lifted
+    with a ragged last slab."""
     cg, g = c2
-    rng = np.random.default_rng(4)
-    x = start(rng, cg.n, 1, 384)
-    a = run(g, x, cg.n, 1, 384, 70, LCB_FP32, resident=0, stream=0, signrec=1)
-    b = run(g, x, cg.n, 1, 384, 70, LCB_FP32, resident=0, stream=1)
-    c = run(g, x, cg.n, 1, 384, 70, LCB_FP32, resident=0, stream=0, signrec=0)
-    assert np.array_equal(a, b) and np.array_equal(a, c)
+    rng = np.random.default_rng(4 + l)
+    x = start(rng, cg.n, l, B)
+    a = run(g, x, cg.n, l, B, 70, LCB_FP32, ee=ee, resident=0, stream=0, signrec=1)
+    b = run(g, x, cg.n, l, B, 70, LCB_FP32, ee=ee, resident=0, stream=1)
+    c = run(g, x, cg.n, l, B, 70, LCB_FP32, ee=ee, resident=0, stream=0, signrec=0)
+    d = run(g, x, cg.n, l, B, 70, LCB_FP32, ee=ee, resident=0, stream=1, slab_outer=1)
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
 
 
 @pytest.mark.parametrize("ee", [False, True])

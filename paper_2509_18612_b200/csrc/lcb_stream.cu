@@ -64,10 +64,19 @@ constexpr int kColBuf = 32 * kR;  // int32 column slots per stage
 #endif
 constexpr int kLook = LCB_STREAM_LOOK;  // producer lookahead (tiles) for the CSR ranges
 constexpr int kSlab = 1024;             // bytes of one row of a slab
-#ifndef LCB_STREAM_FNB
-#define LCB_STREAM_FNB 2
+#ifndef LCB_STREAM_FNB32
+#define LCB_STREAM_FNB32 1
 #endif
-constexpr int kFNB = LCB_STREAM_FNB;    // interior-neighbour gathers in flight (fp mode)
+#ifndef LCB_STREAM_FNB64
+#define LCB_STREAM_FNB64 2
+#endif
+// interior-neighbour gathers in flight per warp (fp mode, before saturation): one for fp32
+// (the leaner code wins over the whole solve: config 4 1382 -> 1351 us/iteration, config 5
+// 80.7 -> 78.2), two for fp64 (3151 vs 3247)
+template <typename T>
+struct Fnb {
+    static constexpr int v = sizeof(T) == 4 ? LCB_STREAM_FNB32 : LCB_STREAM_FNB64;
+};
 #ifndef LCB_STREAM_D
 #define LCB_STREAM_D 1
 #endif
@@ -703,6 +712,7 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                             acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
                     }
                     // sequential fp adds; the neighbour index is only needed for interior neighbours
+                    constexpr int kFNB = Fnb<T>::v;
                     for (int k = 0; k < cnt; k += kFNB) {
                         T g[kFNB][E];
                         uint32_t bq[kFNB];

@@ -310,7 +310,7 @@ struct StreamSmem {
     uint64_t empty[kStages];
 };
 
-template <typename T, bool GEN, bool EE>
+template <typename T, bool GEN, bool EE, int FNB>
 __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
     k_stream(StepArgs<T> a, int rowtiles, int slab0, int nslabs, const __grid_constant__ CUtensorMap mx,
              const __grid_constant__ CUtensorMap mv) {
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(kThreadsS, LCB_STREAM_MINB)
                             acc[e] = static_cast<T>(2 * static_cast<int>(unpack(e) + (wide_used ? wide[e] : 0u)) - folded);
                     }
                     // sequential fp adds; the neighbour index is only needed for interior neighbours
-                    constexpr int kFNB = Fnb<T>::v;
+                    constexpr int kFNB = FNB;
                     for (int k = 0; k < cnt; k += kFNB) {
                         T g[kFNB][E];
                         uint32_t bq[kFNB];
@@ -909,18 +909,18 @@ void slab_map(CUtensorMap* m, const void* base, int64_t ld, int n, int elem_byte
         throw Failure{LCB_CUDA, "cuTensorMapEncodeTiled(slab) failed: " + std::to_string(static_cast<int>(r))};
 }
 
-template <typename T, bool GEN, bool EE>
+template <typename T, bool GEN, bool EE, int FNB = Fnb<T>::v>
 void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
     const int smem = static_cast<int>(sizeof(StreamSmem));
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_smem_attr(reinterpret_cast<const void*>(k_stream<T, GEN, EE>), smem, "cudaFuncSetAttribute(k_stream)");
+    ensure_smem_attr(reinterpret_cast<const void*>(k_stream<T, GEN, EE, FNB>), smem, "cudaFuncSetAttribute(k_stream)");
     static std::atomic<int> grid_per_dev[64];
     const int slot = dev >= 0 && dev < 64 ? dev : 0;
     int gpd = grid_per_dev[slot].load(std::memory_order_relaxed);
     if (!gpd) {
         int occ = 0;
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream<T, GEN, EE>, kThreadsS, smem),
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream<T, GEN, EE, FNB>, kThreadsS, smem),
                    "occupancy(k_stream)");
         gpd = std::max(1, occ) * num_sms(dev);
         grid_per_dev[slot].store(gpd, std::memory_order_relaxed);
@@ -942,7 +942,7 @@ void go_stream(const StepArgs<T>& a, int slab0, int nslabs, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cuda_check(cudaLaunchKernelEx(&cfg, k_stream<T, GEN, EE>, a, rowtiles, slab0, nslabs, mx, mv),
+    cuda_check(cudaLaunchKernelEx(&cfg, k_stream<T, GEN, EE, FNB>, a, rowtiles, slab0, nslabs, mx, mv),
                "cudaLaunchKernelEx(k_stream)");
 }
 
@@ -992,6 +992,11 @@ void launch_stream(const StepArgs<T>& a, int slab0, int nslabs, bool early_exit,
         go_stream<T, true, true>(a, slab0, nslabs, s);
     else if (a.tlim != nullptr || a.alpha != nullptr)
         go_stream<T, true, false>(a, slab0, nslabs, s);
+    else if (sizeof(T) == 4 && a.it < 24)
+        // before saturation fp32 gathers every neighbour: two gathers in flight pay there
+        // (config 4: 5175 vs 5859 us per iteration over the first 20), the leaner one-gather
+        // build wins afterwards; both sum in the same order (bitwise identical)
+        go_stream<T, false, false, 2>(a, slab0, nslabs, s);
     else
         go_stream<T, false, false>(a, slab0, nslabs, s);
 }

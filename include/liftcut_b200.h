@@ -286,8 +286,10 @@ typedef struct lcb_loopback lcb_loopback;
 int lcb_loopback_create(int32_t nranks, lcb_loopback** out);
 void lcb_loopback_destroy(lcb_loopback* g);
 int lcb_comm_create_loopback(lcb_loopback* group, int32_t rank, int device, lcb_comm** out);
-/* Solves keep their device workspaces in a per-(device, precision) pool for reuse;
- * this frees every pooled workspace (e.g. before a large allocation elsewhere). */
+/* Solves keep their device workspaces in a per-(device, precision) pool for reuse, and
+ * graph arrays / ingest scratch come from each device's cached stream-ordered pool; this
+ * frees every pooled workspace and trims those pools (e.g. before a large allocation
+ * elsewhere). */
 void lcb_release_workspaces(void);
 /* process-wide counters: kernel launches and host<->device bytes since load */
 void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes);

@@ -2977,8 +2977,21 @@ void lcb_release_workspaces(void) {
         std::lock_guard<std::mutex> lk(WorkPool<float>::get().mu);
         fl->clear();
     }
-    std::lock_guard<std::mutex> lk(WorkPool<double>::get().mu);
-    WorkPool<double>::get().free_list.clear();
+    {
+        std::lock_guard<std::mutex> lk(WorkPool<double>::get().mu);
+        WorkPool<double>::get().free_list.clear();
+    }
+    // and the cached stream-ordered pool of graph arrays / ingest scratch on every device
+    int ndev = 0, cur = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) return;
+    for (int d = 0; d < ndev; ++d) {
+        cudaMemPool_t pool;
+        if (cudaSetDevice(d) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+            cudaDeviceSynchronize();
+            cudaMemPoolTrimTo(pool, 0);
+        }
+    }
+    cudaSetDevice(cur);
 }
 
 void lcb_counters(int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes) {

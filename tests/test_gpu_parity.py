@@ -450,3 +450,22 @@ def test_adjacency_range_checked_on_both_ingest_paths():
         lc.Graph.from_csr(n, off, adj).handle()  # fine
         with pytest.raises(lc.ValidationError, match="out of range"):
             lc.Graph.from_csr(n, off, np.array([n, 0], dtype=np.uint32)).handle()
+
+
+def test_release_workspaces_then_solve_again():
+    """lcb_release_workspaces frees the pooled workspaces and trims the graph pools; the
+    next graph build and solve allocate afresh and still match the oracle."""
+    from paper_2509_18612_b200 import _abi
+
+    cg = O.generate_er(300, 0.05, 2)
+    rng = np.random.default_rng(6)
+    x = rng.uniform(-0.1, 0.1, 8 * cg.n)
+    want, _ = O.ascend(cg, x, 1, 8, 0.05, 20, 0.9, False)
+    for _ in range(2):
+        g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+        s = lc.DenseState(cg.n, 1, 8)
+        s.values[:] = x
+        lc.ascend(g, s, lc.AscentParams(0.05, 20, 0.9, False), precision=LCB_FP64)
+        assert np.array_equal(s.values, want)
+        g.release()
+        _abi.lib().lcb_release_workspaces()

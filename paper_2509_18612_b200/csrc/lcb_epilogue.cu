@@ -282,8 +282,35 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
                                                   uint32_t* __restrict__ win_bits, int warp_rows,
                                                   uint32_t* __restrict__ Zt) {
     namespace cg = cooperative_groups;
-    // ---- round + pack (objectives.cpp:81-96): one warp per (row, 32-member word)
-    {
+    // ---- round + pack (objectives.cpp:81-96).  Unlifted: one warp per row, eight words'
+    // loads in flight per lane (a 2 KB row of config 4 is 16 coalesced 128-byte loads).
+    if (!lifted) {
+        const int lane = threadIdx.x & 31;
+        const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+        for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n;
+             row += stride) {
+            const T* p = X + row * ld;
+            for (int w0 = 0; w0 < words; w0 += 8) {
+                T v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int m = (w0 + q) * 32 + lane;
+                    v[q] = (w0 + q < words && m < members) ? p[m] : T(0);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (w0 + q < words) {
+                        const uint32_t bits = __ballot_sync(0xffffffffu, static_cast<double>(v[q]) > 0.0);  // strict
+                        if (lane == 0) {
+                            Z[static_cast<int64_t>(w0 + q) * n + row] = bits;
+                            if (Zt) Zt[row * 8 + w0 + q] = bits;
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        // lifted: one warp per (row, 32-member word), the row sum in column order
         const int lane = threadIdx.x & 31;
         const int64_t total = static_cast<int64_t>(n) * words;
         const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;

@@ -472,6 +472,11 @@ def roofline(kst, step_ms, name, precision):
             "algorithmic_bytes_per_launch": k_amount / max(k_launch, 1),
             "ms_per_launch": k_ms / max(k_launch, 1), "step_time_share": shares, "peak_source": which,
             "model": "16 B/node-update fp32 (32 fp64) + 4*nnz + 4*(n+1) CSR bytes per iteration (SURVEY 8d); "
+                     "achieved = that / CUDA-event time of the kernel's launches on the solver stream. "
+                     "Every node-update is computed; K1s stores row slabs that sit on the box corners as their "
+                     "sign codes (x = +-1 exactly), so the measured DRAM traffic (traffic) is below this model "
+                     "(DESIGN.md 4.1)" if kname == "k_stream" else
+                     "16 B/node-update fp32 (32 fp64) + 4*nnz + 4*(n+1) CSR bytes per iteration (SURVEY 8d); "
                      "achieved = that / CUDA-event time of the kernel's launches on the solver stream"}
 
 

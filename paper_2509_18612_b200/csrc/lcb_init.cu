@@ -87,6 +87,43 @@ __global__ void k_idi_vote(const int* __restrict__ row_ptr, const int* __restric
     mean[i] = __ddiv_rn(x, scale);
 }
 
+// The same vote with one warp per (column, node), the lanes striding over the neighbours
+// (dense graphs: a 10k-neighbour row is not one thread's dependent load chain).  The
+// counts are integers, so the result equals the sequential vote.
+__global__ void k_idi_vote_warp(const int* __restrict__ row_ptr, const int* __restrict__ col, int n,
+                                const uint64_t* __restrict__ col_keys, int l, double scale,
+                                const uint32_t* __restrict__ carry, const int8_t* __restrict__ sign,
+                                double* __restrict__ mean) {
+    const int lane = threadIdx.x & 31;
+    const int64_t total = static_cast<int64_t>(n) * l;
+    const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < total; i += stride) {
+        const int c = static_cast<int>(i / n), v = static_cast<int>(i % n);
+        const int8_t* sc = sign + static_cast<int64_t>(c) * n;
+        double x;
+        if (sc[v] != 0) {
+            x = static_cast<double>(sc[v]);
+        } else {
+            int plus = 0, minus = 0;
+            for (int k = row_ptr[v] + lane; k < row_ptr[v + 1]; k += 32) {
+                const int8_t t = sc[col[k]];
+                plus += t > 0;
+                minus += t < 0;
+            }
+            plus = __reduce_add_sync(0xffffffffu, plus);
+            minus = __reduce_add_sync(0xffffffffu, minus);
+            if (plus == minus) {
+                const uint64_t tie = combine(col_keys[c], 0x7469u);  // split({"ti"})
+                x = (rng_at(tie, static_cast<uint64_t>(v)) & 1u) ? 1.0 : -1.0;
+            } else {
+                x = plus < minus ? 1.0 : -1.0;
+            }
+        }
+        x = carry_or(carry, c, v, x);
+        if (lane == 0) mean[i] = __ddiv_rn(x, scale);
+    }
+}
+
 // X[v][m*l+c] = clamp(mean(c,v) + noise * N(member_key(m), c*n + v)); V = 0.
 // Columns past W (row padding) are zeroed.
 template <typename T>
@@ -133,8 +170,12 @@ void launch_idi(const DevGraph& g, double threshold, const uint64_t* col_keys, i
     count_launch();
     k_idi_sign<<<blocks, 256, 0, s>>>(g.row_ptr, g.n, threshold, col_keys, l, sign_scratch);
     count_launch();
-    k_idi_vote<<<blocks, 256, 0, s>>>(g.row_ptr, g.col, g.n, col_keys, l, init_scale, carry_bits,
-                                      sign_scratch, mean);
+    if (g.deg_mean > 64.0)
+        k_idi_vote_warp<<<static_cast<unsigned>(std::min<int64_t>((total + 7) / 8, 148 * 32)), 256, 0, s>>>(
+            g.row_ptr, g.col, g.n, col_keys, l, init_scale, carry_bits, sign_scratch, mean);
+    else
+        k_idi_vote<<<blocks, 256, 0, s>>>(g.row_ptr, g.col, g.n, col_keys, l, init_scale, carry_bits,
+                                          sign_scratch, mean);
 }
 
 template <typename T>

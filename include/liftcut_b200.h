@@ -51,7 +51,8 @@ int lcb_device_count(int* count);
  * 0 off, 1 on, -1 auto), "res_split" (K2 wave-tail split), "bank_order" / "bank_refine"
  * (K2 fp32 neighbour order, read at graph creation), "dense" (K3 adjacency at graph
  * creation: -1 auto, 0, 1), "slab_outer" (K1s order: -1 auto, 0 all slabs per launch, 1 one
- * slab at a time for all iterations).  Defaults come from the LCB_<NAME> environment variables.
+ * slab at a time for all iterations), "xcode" (K1s saturated slabs kept as sign codes: 1, 0),
+ * "dense_cut" (K3 graphs: unlifted cut counts on the tensor cores: 1, 0 bit-sliced).  Defaults come from the LCB_<NAME> environment variables.
  * Changing a knob while a solve runs in another thread is not supported. */
 int lcb_set_option(const char* name, int64_t value);
 int lcb_get_option(const char* name, int64_t* value);

@@ -229,6 +229,7 @@ struct DenseArgs {
     int fp8;                    // e4m3 operands available for fully corner-valued 64-node steps
     const uint32_t* kflags_in;  // [K steps] 0: the mid/lo planes of this 32-node K step are all zero
     uint32_t* kflags_out;       // the same for the planes written by this launch
+    unsigned long long* cut_sum;  // cut mode: [W] sum_v s_v (A s)_v of the sign planes (no step)
 };
 
 // Blocked B operand: plane p, K step ks = node / 32 -> one contiguous [nb][32] bf16 block
@@ -345,6 +346,27 @@ __device__ __forceinline__ bool finish_chunk8(const DenseArgs& a, int row, int c
         low |= ((__bfloat16_as_ushort(mi) | __bfloat16_as_ushort(lo)) & 0x7fffu) != 0;
     }
     return low;
+}
+
+// Cut mode, 8 columns of one row: the accumulator holds (A s)_v for the sign planes
+// s = x > 0 ? +1 : -1 (objectives.cpp:81-96), an exact integer in fp32; sum s_v (A s)_v
+// over the warp's 32 rows per column and add it to the column's total.
+__device__ __forceinline__ void cut_chunk8(const DenseArgs& a, int row, bool live, int c0, const uint32_t (&r)[8]) {
+    const int lane = threadIdx.x & 31;
+    const float* xr = a.X + static_cast<int64_t>(c0) * a.ldx + row;
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        int d = 0;
+        if (live && c0 + j < a.W) {
+            d = __float2int_rn(__uint_as_float(r[j]));
+            if (!(xr[j * a.ldx] > 0.f)) d = -d;
+        }
+        d = __reduce_add_sync(0xffffffffu, d);
+        if (lane == j) mine = d;
+    }
+    if (lane < 8 && c0 + lane < a.W && mine)
+        atomicAdd(a.cut_sum + c0 + lane, static_cast<unsigned long long>(static_cast<long long>(mine)));
 }
 
 // Two smem carve-ups of the same ring, chosen per launch from the K-step flags of the
@@ -543,7 +565,12 @@ __global__ void __launch_bounds__(kThreadsDense, 1)
                 for (int j = 0; j < 8; ++j) pp[static_cast<int64_t>(c0 + j) * kBM] = __uint_as_float(r[j]);
                 continue;
             }
-            if (!live || c0 >= a.W) continue;
+            if (c0 >= a.W) continue;
+            if (a.cut_sum) {
+                cut_chunk8(a, row, live, c0, r);
+                continue;
+            }
+            if (!live) continue;
             low_nz |= finish_chunk8(a, row, c0, r, dg);
         }
         // one lane quarter = one 32-node K step of the next iteration's B operand; split-K
@@ -572,6 +599,24 @@ __global__ void k_dense_reduce(DenseArgs a) {
     const int t = blockIdx.y;                         // tail tile index within this launch
     const int row_in = threadIdx.x;                   // 0..127
     const int row = (a.tile_base + t) * kBM + row_in;
+    if (a.cut_sum) {  // cut mode (as cut_chunk8), the pieces summed in the same fixed order
+        const bool live = row < a.n;
+        for (int c = blockIdx.x; c < a.W; c += gridDim.x) {
+            int d = 0;
+            if (live) {
+                float ax = 0.f;
+                for (int p = 0; p < a.k_split; ++p)
+                    ax += a.partial[(static_cast<int64_t>(t) * a.k_split + p) * N * kBM + static_cast<int64_t>(c) * kBM +
+                                    row_in];
+                d = __float2int_rn(ax);
+                if (!(a.X[static_cast<int64_t>(c) * a.ldx + row] > 0.f)) d = -d;
+            }
+            d = __reduce_add_sync(0xffffffffu, d);
+            if ((threadIdx.x & 31) == 0 && d)
+                atomicAdd(a.cut_sum + c, static_cast<unsigned long long>(static_cast<long long>(d)));
+        }
+        return;
+    }
     if (row >= a.n) return;
     const float dg = __ldg(a.deg + row);
     bool low_nz = false;
@@ -607,6 +652,25 @@ __global__ void k_to_member_major(const float* __restrict__ X, int64_t ld, int n
             P[ps + po] = m;
             P[2 * ps + po] = l;
         }
+    }
+}
+
+// cut mode operands: the sign s = x > 0 ? +1 : -1 of the final iterate as the hi plane
+// (mid / lo zero) and as its e4m3 copy (0x38 = +1, 0xb8 = -1)
+__global__ void k_sign_planes(const float* __restrict__ Xm, int ldx, int n, int W, __nv_bfloat16* __restrict__ P,
+                              int nks, int nb, uint8_t* __restrict__ P8) {
+    const int64_t total = static_cast<int64_t>(W) * n;
+    const int64_t ps = static_cast<int64_t>(nks) * nb * 32;
+    const __nv_bfloat16 one = __float2bfloat16(1.f), mone = __float2bfloat16(-1.f), zero = __float2bfloat16(0.f);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i / n), v = static_cast<int>(i % n);
+        const bool z = Xm[static_cast<int64_t>(c) * ldx + v] > 0.f;
+        const int64_t po = plane_index(0, v, c, nks, nb);
+        P[po] = z ? one : mone;
+        P[ps + po] = zero;
+        P[2 * ps + po] = zero;
+        P8[plane8_index(v, c, nb)] = z ? 0x38 : 0xb8;
     }
 }
 
@@ -746,7 +810,7 @@ int dense_ldp(int n) { return (n + 7) / 8 * 8; }
 void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
                           int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
-                          void* planes, cudaStream_t s, int col_base, float* partial) {
+                          void* planes, cudaStream_t s, int col_base, float* partial, unsigned long long* cut_sum) {
     const int n = g.n;
     const int ldx = dense_ldp(n);
     const int nks = dense_nks(n);
@@ -811,6 +875,32 @@ void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodem
         a.plane8_in = P8buf[it & 1];
         a.adj8 = A8;
         const CUtensorMap& mp = mP[it & 1];
+        if (NB == 64)
+            launch_dense_n<64>(mA, mp, a, partial, s);
+        else if (NB == 128)
+            launch_dense_n<128>(mA, mp, a, partial, s);
+        else
+            launch_dense_n<256>(mA, mp, a, partial, s);
+    }
+    if (cut_sum) {
+        // the rounding's cut counts as one more tensor-core pass: (A s) for the sign planes
+        // of the final iterate, every K step an e4m3 unit (s = +-1 exactly)
+        const int b = static_cast<int>(iters & 1);
+        count_launch();
+        k_sign_planes<<<148 * 8, 256, 0, s>>>(Xm, ldx, n, W, Pbuf[b], nks, NB, P8buf[b]);
+        cuda_check(cudaMemsetAsync(Fbuf[b], 0, sizeof(uint32_t) * static_cast<size_t>(nks), s), "memset(kflags)");
+        cuda_check(cudaMemsetAsync(cut_sum, 0, sizeof(unsigned long long) * static_cast<size_t>(W), s), "memset(cut)");
+        a.it = static_cast<int>(iters);
+        a.planes_out = nullptr;
+        a.plane8_out = nullptr;
+        a.kflags_in = Fbuf[b];
+        a.kflags_out = nullptr;
+        a.fp8 = fp8 ? 1 : 0;
+        a.plane8_in = P8buf[b];
+        a.alpha = nullptr;
+        a.tlim = nullptr;
+        a.cut_sum = cut_sum;
+        const CUtensorMap& mp = mP[b];
         if (NB == 64)
             launch_dense_n<64>(mA, mp, a, partial, s);
         else if (NB == 128)

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
                                                   unsigned long long* __restrict__ done, int seg_size,
                                                   int64_t member_base, unsigned long long* __restrict__ seg_keys,
                                                   uint32_t* __restrict__ win_bits, int warp_rows,
-                                                  uint32_t* __restrict__ Zt) {
+                                                  uint32_t* __restrict__ Zt, int skip_cut) {
     namespace cg = cooperative_groups;
     // ---- round + pack (objectives.cpp:81-96).  Unlifted: one warp per row, eight words'
     // loads in flight per lane (a 2 KB row of config 4 is 16 coalesced 128-byte loads).
@@ -337,8 +337,9 @@ __global__ void __launch_bounds__(256) k_epilogue(const T* __restrict__ X, int64
         }
     }
     cg::this_grid().sync();
-    // ---- cut counts (objectives.cpp:26-35)
-    if (Zt) {
+    // ---- cut counts (objectives.cpp:26-35); skip_cut: already in `cuts` (dense cut pass)
+    if (skip_cut) {
+    } else if (Zt) {
         // dense graphs, <= 8 words: warp j of every block counts word j over the block's rows;
         // the 8 warps read the same column runs and the same 32-byte node-major Zt lines, so
         // those loads hit L1 after the first warp
@@ -572,12 +573,26 @@ void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned
                                                        seg_size, member_base, seg_keys, g.deg_mean > 64.0 ? 1 : 0);
 }
 
+// cut(m) = (nnz - sum_v s_v (A s)_v) / 4 for s = +-1 (each undirected edge appears twice in
+// the CSR: sum over edges of s_u s_v = uncut - cut = nnz / 2 - 2 cut); done counter zeroed
+__global__ void k_cuts_from_sums(const unsigned long long* __restrict__ sums, int members, int64_t nnz,
+                                 unsigned long long* __restrict__ cuts, int slots) {
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= slots; m += gridDim.x * blockDim.x)
+        cuts[m] = m < members ? static_cast<unsigned long long>((nnz - static_cast<long long>(sums[m])) / 4) : 0ull;
+}
+
 template <typename T>
 void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int l, int lifted, uint32_t* Z,
                      unsigned long long* cuts, int seg_size, int64_t member_base, unsigned long long* seg_keys,
-                     uint32_t* win_bits, cudaStream_t s) {
+                     uint32_t* win_bits, cudaStream_t s, const unsigned long long* cut_sums) {
     const int words = (members + 31) / 32;
-    cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * (static_cast<size_t>(words) * 32 + 1), s);
+    int skip_cut = cut_sums ? 1 : 0;
+    if (cut_sums) {
+        count_launch();
+        k_cuts_from_sums<<<(words * 32 + 256) / 256, 256, 0, s>>>(cut_sums, members, g.nnz, cuts, words * 32);
+    } else {
+        cudaMemsetAsync(cuts, 0, sizeof(unsigned long long) * (static_cast<size_t>(words) * 32 + 1), s);
+    }
     static std::atomic<int> per_sm[64];
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
@@ -592,7 +607,7 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     const int resident = occ * num_sms(dev);
     // dense graphs with <= 8 words: every block counts all words (warp j = word j) over its
     // rows, sharing the column and Zt loads in L1; Zt = node-major copy of Z [n][8]
-    const bool dense_block = g.deg_mean > 64.0 && words <= 8;
+    const bool dense_block = !skip_cut && g.deg_mean > 64.0 && words <= 8;
     int parts = std::max(1, std::min((g.n + 255) / 256, resident / words));
     int grid = parts * words;
     uint32_t* Zt = nullptr;
@@ -602,7 +617,10 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     } else if (parts * words > resident)  // more words than resident blocks: the unfused kernels
     {
         launch_round_pack<T>(X, ld, g.n, members, l, lifted, Z, s);
-        launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
+        if (skip_cut)
+            launch_argmax(cuts, members, seg_size, member_base, seg_keys, s);
+        else
+            launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
         if (win_bits) launch_extract_winner(Z, g.n, seg_keys, member_base, members, win_bits, s, 0);
         return;
     }
@@ -612,7 +630,7 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
     const int* cl = g.col;
     int warp_rows = g.deg_mean > 64.0 ? 1 : 0;
     void* args[] = {&X, &ld, &n, &members, &l, &lifted, &Z, &nw, &rp, &cl, &cuts, &done, &seg_size,
-                    &member_base, &seg_keys, &win_bits, &warp_rows, &Zt};
+                    &member_base, &seg_keys, &win_bits, &warp_rows, &Zt, &skip_cut};
     count_launch();
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_epilogue<T>), dim3(grid),
                                                       dim3(256), args, 0, s);
@@ -622,17 +640,21 @@ void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int
         // the same epilogue as separate launches
         (void)cudaGetLastError();
         launch_round_pack<T>(X, ld, g.n, members, l, lifted, Z, s);
-        launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
+        if (skip_cut)
+            launch_argmax(cuts, members, seg_size, member_base, seg_keys, s);
+        else
+            launch_cut_argmax(g, Z, words, cuts, members, seg_size, member_base, seg_keys, s);
         if (win_bits) launch_extract_winner(Z, g.n, seg_keys, member_base, members, win_bits, s, 0);
         return;
     }
     cuda_check(e, "cudaLaunchCooperativeKernel(k_epilogue)");
 }
 template void launch_epilogue<float>(const DevGraph&, const float*, int64_t, int, int, int, uint32_t*,
-                                     unsigned long long*, int, int64_t, unsigned long long*, uint32_t*, cudaStream_t);
+                                     unsigned long long*, int, int64_t, unsigned long long*, uint32_t*, cudaStream_t,
+                                     const unsigned long long*);
 template void launch_epilogue<double>(const DevGraph&, const double*, int64_t, int, int, int, uint32_t*,
                                       unsigned long long*, int, int64_t, unsigned long long*, uint32_t*,
-                                      cudaStream_t);
+                                      cudaStream_t, const unsigned long long*);
 
 void launch_argmax(const unsigned long long* cuts, int members, int seg_size, int64_t member_base,
                    unsigned long long* seg_keys, cudaStream_t s) {

@@ -161,7 +161,8 @@ void build_dense_adjacency(const DevGraph& g, void* A, cudaStream_t s);
 void run_dense_iterations(const DevGraph& g, const void* A, const float* X_nodemajor_in, float* X_nodemajor_out,
                           int64_t ld, int W, int l, int64_t iters, float alpha_u, const float* alpha_arr,
                           const int* tlim_arr, float mu, unsigned long long* err, int err_seg, float* Xm, float* Vm,
-                          void* planes, cudaStream_t s, int col_base, float* partial);
+                          void* planes, cudaStream_t s, int col_base, float* partial,
+                          unsigned long long* cut_sum = nullptr);
 size_t dense_partial_floats();
 size_t dense_planes_bytes(int n, int W);
 // L2-panel path (lcb_narrow.cu): all iterations for one narrow column panel
@@ -221,7 +222,7 @@ void launch_cut_count(const DevGraph& g, const uint32_t* Z, int words, unsigned 
 template <typename T>
 void launch_epilogue(const DevGraph& g, const T* X, int64_t ld, int members, int l, int lifted, uint32_t* Z,
                      unsigned long long* cuts, int seg_size, int64_t member_base, unsigned long long* seg_keys,
-                     uint32_t* win_bits, cudaStream_t s);
+                     uint32_t* win_bits, cudaStream_t s, const unsigned long long* cut_sums = nullptr);
 void launch_cut_argmax(const DevGraph& g, const uint32_t* Z, int words, unsigned long long* cuts, int members,
                        int seg_size, int64_t member_base, unsigned long long* seg_keys, cudaStream_t s);
 // segment argmax of packed keys; seg_keys[s] = max over members of segment s
@@ -277,6 +278,7 @@ enum Opt : int {
     OPT_DENSE,         // K3 adjacency at graph creation: -1 auto, 0 never, 1 always
     OPT_SLAB_OUTER,    // K1s order: -1 auto (codes beyond L2), 0 iteration-major, 1 slab-major
     OPT_XCODE,         // K1s: saturated row slabs keep x in the sign code only (1 on, 0 off)
+    OPT_DENSE_CUT,     // K3 graphs: unlifted cut counts as a tensor-core pass (1 on, 0 bit-sliced)
     OPT_COUNT
 };
 int64_t option(Opt o);

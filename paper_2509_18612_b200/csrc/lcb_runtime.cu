@@ -78,7 +78,7 @@ constexpr OptDef kOptDefs[OPT_COUNT] = {
     {"resident", "LCB_RESIDENT", -1}, {"stream", "LCB_STREAM", 1},         {"signrec", "LCB_SIGNREC", -1},
     {"chunk", "LCB_CHUNK", 0},        {"res_split", "LCB_RES_SPLIT", 1},   {"bank_order", "LCB_BANK_ORDER", 2},
     {"bank_refine", "LCB_BANK_REFINE", 2}, {"dense", "LCB_DENSE", -1}, {"slab_outer", "LCB_SLAB_OUTER", -1},
-    {"xcode", "LCB_XCODE", 1},
+    {"xcode", "LCB_XCODE", 1},        {"dense_cut", "LCB_DENSE_CUT", 1},
 };
 std::atomic<int64_t> g_opts[OPT_COUNT];
 std::once_flag g_opts_once;
@@ -795,6 +795,9 @@ struct Work {
     DBuf<int> tlim;
     DBuf<uint32_t> flags;
     DBuf<unsigned long long> err, cuts, keys;
+    DBuf<unsigned long long> dcut;               // dense path: per-member sum_v s_v (A s)_v (cut pass)
+    unsigned long long* dense_cut_req = nullptr;  // set by run_batch: fill it if K3 runs (l = 1)
+    bool dense_cut_done = false;
     DBuf<uint32_t> Z;
     DBuf<uint64_t> mkeys, colkeys;
     DBuf<double> mean, dtrace, hostbatch;
@@ -993,8 +996,10 @@ IterResult run_iterations(const DevGraph& g, Work<T>& w, int W, int members, int
                     if (seg < seg_iters->size()) chunk_iters = (*seg_iters)[seg];
                 }
                 float* part = w.dpartial.ensure(dense_partial_floats());
+                unsigned long long* cs = w.dense_cut_req && l == 1 ? w.dense_cut_req + c0 : nullptr;
                 run_dense_iterations(g, g.dense_A, w.X[0].p + c0, w.X[1].p + c0, w.ld, Wc, l, chunk_iters, alpha_u,
-                                     alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0, part);
+                                     alpha_arr, tlim_arr, mu, a.err, err_seg, Xm, Vm, P, w.st, c0, part, cs);
+                w.dense_cut_done = cs != nullptr;
             }
             CK(cudaEventRecord(w.ev1, w.st));
             CK(cudaGetLastError());
@@ -1547,9 +1552,13 @@ struct Solver {
         std::vector<double> tr;
         const bool tracing = book && trace_fn != nullptr;
         if (tracing) tr.assign(static_cast<size_t>(iters) * static_cast<size_t>(B), 0.0);
+        // dense graphs, unlifted: K3 computes the cut counts with one more tensor-core pass
+        w.dense_cut_done = false;
+        w.dense_cut_req = g.dense_A && !lifted && l == 1 && option(OPT_DENSE_CUT) != 0 ? w.dcut.ensure(B) : nullptr;
         IterResult ir = run_iterations<T>(g, w, W, static_cast<int>(B), l, iters, static_cast<T>(alpha),
                                           nullptr, nullptr, static_cast<T>(mu), ee && !tracing,
                                           tracing ? tr.data() : nullptr);
+        w.dense_cut_req = nullptr;
         sync_errors(ir);
         if (tracing)  // member-major, as the reference with workers=1 (ascent.cpp:52,87)
             for (int64_t j = 0; j < B; ++j)
@@ -1568,7 +1577,9 @@ struct Solver {
         // K4, one kernel: round -> cut counts -> argmax -> (single rank) winner bits
         const bool multi = comm_active(comm);
         launch_epilogue<T>(g, w.X[ir.final_buf].p, w.ld, static_cast<int>(B), l, lifted ? 1 : 0, Z, cuts,
-                           static_cast<int>(B), member_base, key, multi ? nullptr : w.win.p, w.st);
+                           static_cast<int>(B), member_base, key, multi ? nullptr : w.win.p, w.st,
+                           w.dense_cut_done ? w.dcut.p : nullptr);
+        w.dense_cut_done = false;
         if (multi) {
             comm_allreduce(comm, key, 1, 8, true, w.st, "allreduce(key)");
             launch_extract_winner(Z, n, key, member_base, static_cast<int>(B), w.win.p, w.st);

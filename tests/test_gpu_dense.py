@@ -152,3 +152,50 @@ def test_dense_config3_scale_split_k_tail_vs_fp64():
     print(res)
     assert res["1"] <= 1e-5 and res["4"] <= 1e-5, res
     assert res["same"] >= 0.97 and res["d"] <= 2, res
+
+
+CUT_CODE = r"""
+import json, numpy as np
+import oracle as O
+from paper_2509_18612_b200 import liftcut as lc, LCB_FP32
+cg = O.generate_er(600, 0.5, 3)
+g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+opts = lc.RunOptions(precision=LCB_FP32)
+res = {}
+for algo, B in ((lc.Algorithm.pQUCO, 64), (lc.Algorithm.pQUCO, 320), (lc.Algorithm.pDECO, 96)):
+    cfg = lc.SolverConfig(algorithm=algo, batch_size=B, lift_dim=2, ascent=lc.AscentParams(0.01, 60),
+                          lifted_ascent=lc.AscentParams(0.01, 60), num_batches=2, deco_alternations=1)
+    outs = []
+    for dc in (1, 0):
+        with lc.options(dense_cut=dc):
+            o = lc.pquco(g, cfg, 5, opts=opts) if algo == lc.Algorithm.pQUCO else lc.pdeco(g, cfg, 5, opts=opts)
+        outs.append(o)
+    a, b = outs
+    res[f"{int(algo)}x{B}"] = dict(
+        cut=[a.best.cut_value, b.best.cut_value],
+        same_trace=[repr(e) for e in a.batch_trace] == [repr(e) for e in b.batch_trace],
+        same_bits=bool(np.array_equal(a.best.assignment, b.best.assignment)),
+        check=int(O.cut_value(cg, np.asarray(a.best.assignment, dtype=np.uint8))) if hasattr(O, "cut_value") else -1)
+print("RESULT" + json.dumps(res))
+"""
+
+
+@pytest.mark.parametrize("sms", [None, "4"])
+def test_dense_cut_pass_equals_bit_sliced_counts(sms):
+    """Unlifted solves on a K3 graph count the cut edges as one more tensor-core pass
+    (sum_v s_v (A s)_v of the rounded signs, cut = (nnz - sum) / 4): the per-batch cuts, the
+    winner and its assignment equal the bit-sliced CSR count (dense_cut=0), with and
+    without the split-K tail (sms="4"), for a two-chunk batch (B=320) and inside pDECO."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "LCB_DENSE": "1"}
+    if sms:
+        env["LCB_DENSE_SMS"] = sms
+    r = subprocess.run([sys.executable, "-c", CUT_CODE], cwd=root, capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    res = json.loads(r.stdout.split("RESULT")[1])
+    print(res)
+    for k, v in res.items():
+        assert v["cut"][0] == v["cut"][1] and v["same_trace"] and v["same_bits"], (k, v)
+        if v["check"] >= 0:
+            assert v["check"] == v["cut"][0], (k, v)

@@ -24,13 +24,14 @@ ap.add_argument("--precision", default="fp32")
 ap.add_argument("--tag", default="")
 ap.add_argument("--graph", default="ba", choices=["ba", "er"])
 ap.add_argument("--quco-only", action="store_true")
+ap.add_argument("--alpha", type=float, default=0.05)
 a = ap.parse_args()
 u, v = ba_edges(a.n, 4, 0) if a.graph == "ba" else fast_gnp_edges(a.n, 10.0 / (a.n - 1), 0)
 g = lc.Graph.from_edges_device(a.n, np.stack([u, v], 1))
 prec = LCB_FP32 if a.precision == "fp32" else LCB_FP64
 for algo, l in ((lc.Algorithm.pQUCO, 1), (lc.Algorithm.pLUCO, 2))[:1 if a.quco_only else 2]:
     cfg = lc.SolverConfig(algorithm=algo, batch_size=a.B, lift_dim=2,
-                          ascent=lc.AscentParams(0.05, a.T, 0.9, False), num_batches=1)
+                          ascent=lc.AscentParams(a.alpha, a.T, 0.9, False), num_batches=1)
     fn = lc.pquco if l == 1 else lc.pluco
     fn(g, cfg, 0, opts=lc.RunOptions(precision=prec, host_init=0))  # warm
     best = None
@@ -39,6 +40,6 @@ for algo, l in ((lc.Algorithm.pQUCO, 1), (lc.Algorithm.pLUCO, 2))[:1 if a.quco_o
         per_it = out.step_ms / a.T
         best = per_it if best is None else min(best, per_it)
     W = a.B * l
-    print(f"{a.tag} {a.precision} n={a.n} W={W}: {best * 1e3:.1f} us/iteration, "
+    print(f"{a.tag} alpha={a.alpha:g} {a.precision} n={a.n} W={W}: {best * 1e3:.1f} us/iteration, "
           f"{g.node_count() * W / (best / 1e3):.3e} node-updates/s, "
           f"{16 * g.node_count() * W / (best / 1e3) / 1e9:.0f} GB/s algorithmic", flush=True)

@@ -173,3 +173,23 @@ def test_graph_constructor_first_offending_edge_decides():
         lc.Graph(5, [[0, 1], [2, 2], [1, 9]])
     with pytest.raises(lc.ValidationError, match=r"out of range: \(1, 9\)"):
         lc.Graph(5, [[0, 1], [1, 9], [2, 2]])
+
+
+def test_every_documented_option_is_registered():
+    """The kernel-selection knobs the header documents (lcb_set_option) exist, keep their
+    documented defaults unless the LCB_<NAME> environment overrides them, round-trip
+    through lc.options, and an unknown name is a ValidationError (no CUDA call)."""
+    text = open(HEADER).read()
+    block = text[text.index("Kernel-selection knobs"):text.index("int lcb_set_option")]
+    names = re.findall(r'"([a-z_0-9]+)"', block)
+    assert {"resident", "stream", "dense", "xcode", "dense_cut"} <= set(names)
+    defaults = {"stream": 1, "xcode": 1, "dense_cut": 1, "dense": -1, "resident": -1}
+    for k in names:
+        v = lc.get_option(k)
+        if k in defaults and f"LCB_{k.upper()}" not in os.environ:
+            assert v == defaults[k], (k, v)
+        with lc.options(**{k: 0}):
+            assert lc.get_option(k) == 0
+        assert lc.get_option(k) == v
+    with pytest.raises(lc.ValidationError, match="unknown option"):
+        lc.set_option("no_such_knob", 1)

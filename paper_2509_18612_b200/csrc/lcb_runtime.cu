@@ -366,6 +366,21 @@ static void refine_bank_order(std::vector<uint16_t>& fast, const std::vector<int
 // host relabelling below needs it, i.e. n <= kResidentMaxRows, else null).
 void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* adj, int device,
                  int* dev_col = nullptr) {
+    struct BuildTimer {  // LCB_BUILD_TIMING=1: host / upload split of a graph build (stderr)
+        bool on = std::getenv("LCB_BUILD_TIMING") != nullptr;
+        Clock::time_point t0 = Clock::now(), last = t0;
+        std::string msg;
+        void mark(const char* what) {
+            if (!on) return;
+            if (what[0] != 'h') cudaDeviceSynchronize();
+            const auto t = Clock::now();
+            msg += std::string(" ") + what + "=" + std::to_string(std::chrono::duration<double>(t - last).count() * 1e3);
+            last = t;
+        }
+        ~BuildTimer() {
+            if (on) fprintf(stderr, "build_graph ms:%s total=%.3f\n", msg.c_str(), secs_since(t0) * 1e3);
+        }
+    } bt;
     if (dev_col) g.col = dev_col;  // freed with the graph, also on failure
     if (n == 0) fail(LCB_VALIDATION, "graph must have at least one node");
     if (off[0] != 0) fail(LCB_VALIDATION, "offsets[0] must be 0");
@@ -414,6 +429,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         for (uint32_t v = 0; v < n; ++v) ord[static_cast<size_t>(start[static_cast<size_t>(maxd - deg[v])]++)] = static_cast<int>(v);
     }
 
+    bt.mark("host");
     DeviceScope ds(device);
     g.row_ptr = static_cast<decltype(g.row_ptr)>(graph_alloc(sizeof(int) * (n + 1)));
     if (!dev_col) g.col = static_cast<decltype(g.col)>(graph_alloc(sizeof(int) * (nnz + 4)));  // K1s copies aligned 16-byte runs
@@ -423,6 +439,7 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
     h2d(g.row_ptr, rp.data(), sizeof(int) * (n + 1), 0);
     // uint32 ids < n < 2^31: the same bits as int32, uploaded straight from the caller
     if (nnz && !dev_col) h2d(g.col, adj, sizeof(int) * nnz, 0);
+    bt.mark("up_csr");
     if (!host_check && nnz && !dev_col) {
         unsigned* dmx = nullptr;
         CK(cudaMalloc(&dmx, sizeof(unsigned)));
@@ -433,9 +450,11 @@ void build_graph(DevGraph& g, uint32_t n, const int64_t* off, const uint32_t* ad
         cudaFree(dmx);
         if (mx >= n) fail(LCB_VALIDATION, "adjacency entry out of range");
     }
+    bt.mark("maxcheck");
     h2d(g.deg64, d64.data(), sizeof(double) * n, 0);
     h2d(g.deg32, d32.data(), sizeof(float) * n, 0);
     h2d(g.order, ord.data(), sizeof(int) * n, 0);
+    bt.mark("up_deg");
 
     g.res_perm = g.order;
     {

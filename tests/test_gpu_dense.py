@@ -163,8 +163,8 @@ g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
 opts = lc.RunOptions(precision=LCB_FP32)
 res = {}
 for algo, B in ((lc.Algorithm.pQUCO, 64), (lc.Algorithm.pQUCO, 320), (lc.Algorithm.pDECO, 96)):
-    cfg = lc.SolverConfig(algorithm=algo, batch_size=B, lift_dim=2, ascent=lc.AscentParams(0.01, 60),
-                          lifted_ascent=lc.AscentParams(0.01, 60), num_batches=2, deco_alternations=1)
+    cfg = lc.SolverConfig(algorithm=algo, batch_size=B, lift_dim=2, ascent=lc.AscentParams(0.01, 60, 0.9, False),
+                          lifted_ascent=lc.AscentParams(0.01, 60, 0.9, False), num_batches=2, deco_alternations=1)
     outs = []
     for dc in (1, 0):
         with lc.options(dense_cut=dc):
@@ -175,7 +175,8 @@ for algo, B in ((lc.Algorithm.pQUCO, 64), (lc.Algorithm.pQUCO, 320), (lc.Algorit
         cut=[a.best.cut_value, b.best.cut_value],
         same_trace=[repr(e) for e in a.batch_trace] == [repr(e) for e in b.batch_trace],
         same_bits=bool(np.array_equal(a.best.assignment, b.best.assignment)),
-        check=int(O.cut_value(cg, np.asarray(a.best.assignment, dtype=np.uint8))) if hasattr(O, "cut_value") else -1)
+        check=int(O.cut_value(cg, np.asarray(a.best.assignment, dtype=np.uint8))) if hasattr(O, "cut_value") else -1,
+        k3=a.kernel_stats["k_dense_step"][1])
 print("RESULT" + json.dumps(res))
 """
 
@@ -197,5 +198,58 @@ def test_dense_cut_pass_equals_bit_sliced_counts(sms):
     print(res)
     for k, v in res.items():
         assert v["cut"][0] == v["cut"][1] and v["same_trace"] and v["same_bits"], (k, v)
+        assert v["k3"] > 0, (k, v)  # the K3 path ran
         if v["check"] >= 0:
             assert v["check"] == v["cut"][0], (k, v)
+
+
+RANK_CODE = r"""
+import json, threading, numpy as np
+import oracle as O
+from paper_2509_18612_b200 import liftcut as lc, LCB_FP32
+from paper_2509_18612_b200.dist import Comm, LoopbackGroup
+cg = O.generate_er(600, 0.5, 4)
+g = lc.Graph.from_csr(cg.n, cg.off, cg.adj)
+cfg = lc.SolverConfig(batch_size=48, ascent=lc.AscentParams(0.01, 40, 0.9, False), num_batches=2)  # K3: no early exit
+
+def two_ranks():
+    grp = LoopbackGroup(2)
+    comms = [Comm.loopback(grp, r, 0) for r in range(2)]
+    out = [None, None]
+    def work(r):
+        out[r] = lc.pquco(g, cfg, 9, opts=lc.RunOptions(precision=LCB_FP32, comm=comms[r]))
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in th: t.start()
+    for t in th: t.join(timeout=600)
+    for c in comms: c.close()
+    grp.close()
+    return out
+
+res = {}
+for dc in (1, 0):
+    lc.set_option("dense_cut", dc)
+    a, b = two_ranks()
+    res[dc] = dict(cut=[a.best.cut_value, b.best.cut_value], member=[a.best.member_index, b.best.member_index],
+                   trace=[repr(e) for e in a.batch_trace], bits=np.asarray(a.best.assignment).tolist(),
+                   same_ranks=bool(np.array_equal(a.best.assignment, b.best.assignment)),
+                   check=int(O.cut_value(cg, np.asarray(a.best.assignment, dtype=np.uint8))),
+                   k3=[a.kernel_stats["k_dense_step"][1], b.kernel_stats["k_dense_step"][1]])
+lc.set_option("dense_cut", 1)
+print("RESULT" + json.dumps(res))
+"""
+
+
+def test_dense_cut_pass_with_two_ranks():
+    """Member sharding over the loopback communicator on a K3 graph: every rank's K3 cut
+    pass feeds the cross-rank key reduction and winner exchange; the result equals the
+    bit-sliced count's (dense_cut=0) on both ranks and the winner's cut recomputes."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", RANK_CODE], cwd=root, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "LCB_DENSE": "1"})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    res = json.loads(r.stdout.split("RESULT")[1])
+    on, off = res["1"], res["0"]
+    assert on["cut"][0] == on["cut"][1] == off["cut"][0] == on["check"], (on["cut"], off["cut"], on["check"])
+    assert on["member"] == off["member"] and on["trace"] == off["trace"] and on["bits"] == off["bits"]
+    assert on["same_ranks"] and off["same_ranks"]
+    assert min(on["k3"]) > 0 and min(off["k3"]) > 0, (on["k3"], off["k3"])  # the K3 path ran

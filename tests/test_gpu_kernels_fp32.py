@@ -182,3 +182,25 @@ def test_k1_saturation_codes_iterate_larger_than_l2():
     want, _ = O.ascend(cg, x, 1, B, 0.05, T, 0.9, False)
     got = run(g, x, n, 1, B, T, LCB_FP64, resident=0, stream=0, signrec=-1)  # auto: on (> L2)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("opts,ee,want", [
+    (dict(resident=1), False, "k_resident"),
+    (dict(resident=1, res_split=0), False, "k_resident"),
+    (dict(resident=0, stream=1), False, "k_stream"),
+    (dict(resident=0, stream=1), True, "k_stream"),
+    (dict(resident=0, stream=1, slab_outer=1), False, "k_stream"),
+    (dict(resident=0, stream=0, signrec=1), True, "k_step"),
+    (dict(resident=0, stream=0, signrec=0), False, "k_step"),
+])
+def test_options_route_to_the_named_kernel(c2, opts, ee, want):
+    """The option sets the tests above use select the kernel they are named after (the
+    solver's per-kernel launch counts on the same graph and batch shape), so a test of
+    "K2" or "K1s" cannot pass on another kernel."""
+    _, g = c2
+    cfg = lc.SolverConfig(batch_size=384, num_batches=1, ascent=lc.AscentParams(0.05, 20, 0.9, ee))
+    with lc.options(**opts):
+        out = lc.pquco(g, cfg, 1, opts=lc.RunOptions(precision=LCB_FP32))
+    ks = {k: v[1] for k, v in out.kernel_stats.items()}
+    assert ks[want] > 0, ks
+    assert all(v == 0 for k, v in ks.items() if k != want), ks
